@@ -1,0 +1,742 @@
+// docp_cuda.cu — host driver and C ABI (include/docp_cuda.h) of the
+// B200-native DiffMPC hot path: a batch object holding every problem's state
+// in HBM, the SQP loop (sqp.hpp:213-261) and the backward pass
+// (backward.hpp:27-50) driven from C++, and the five kernels K1–K4 (+K5's
+// reduction for the gradient sum; the NCCL exchange is done by the caller).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "families.cuh"
+#include "k_assemble.cuh"
+#include "k_pcg.cuh"
+#include "k_step.cuh"
+
+using namespace docp_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_pcg_invocations{0};
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(DOCP_CUDA_ERROR, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                                       \
+  do {                                                                                       \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                      \
+    cudaError_t e_ = cudaGetLastError();                                                     \
+    if (e_ != cudaSuccess) return fail(DOCP_CUDA_ERROR, "kernel launch: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+}  // namespace
+
+struct docp_batch {
+  docp_problem prob{};
+  Dims d{};
+  int B = 0;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  View v{};
+  // work lists: all problems, and two ping-pong active lists
+  int* all_list = nullptr;
+  int* list[2] = {nullptr, nullptr};
+  int* counts = nullptr;  // [0] all, [1] list0, [2] list1, [3] pcg queue counter
+  int* h_count = nullptr; // pinned
+  std::vector<void*> allocs;
+  int max_hist = 0;
+  double last_eps_pd = 1e-6;
+
+  ~docp_batch() {
+    for (void* p : allocs) cudaFree(p);
+    if (h_count) cudaFreeHost(h_count);
+  }
+};
+
+namespace {
+
+template <class T>
+int dalloc(docp_batch* b, T** out, size_t count) {
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  CUDA_TRY(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)));
+  b->allocs.push_back(p);
+  *out = static_cast<T*>(p);
+  return DOCP_OK;
+}
+
+int ensure_hist(docp_batch* b, int n) {
+  if (n <= b->max_hist) return DOCP_OK;
+  int rc;
+  if ((rc = dalloc(b, &b->v.pcg_hist, static_cast<size_t>(b->B) * n))) return rc;
+  if ((rc = dalloc(b, &b->v.step_sizes, static_cast<size_t>(b->B) * n))) return rc;
+  b->max_hist = n;
+  b->v.max_hist = n;
+  return DOCP_OK;
+}
+
+int grid_for(long items, int threads, int cap_blocks = 1 << 20) {
+  long g = (items + threads - 1) / threads;
+  return static_cast<int>(std::max<long>(1, std::min<long>(g, cap_blocks)));
+}
+
+// ---------------------------------------------------------------- kernels of the driver
+__global__ void init_solve_kernel(View v, int* __restrict__ list, int* __restrict__ count) {
+  const Dims d = v.d;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < v.B; p += gridDim.x * blockDim.x) {
+    bool fin = true;
+    const double* z = v.z + static_cast<long>(p) * d.nz;
+    const double* l = v.lam + static_cast<long>(p) * d.nl;
+    for (int e = 0; e < d.nz; ++e) fin = fin && isfinite(z[e]);
+    for (int e = 0; e < d.nl; ++e) fin = fin && isfinite(l[e]);
+    v.mu[p] = 1.0;
+    v.sqp_iters[p] = 0;
+    v.converged[p] = 0;
+    v.kkt[p] = 0.0;
+    if (fin) {
+      set_status(v.status + p, DOCP_OK, DOCP_AT_NONE, 0);
+      list[atomicAdd(count, 1)] = p;
+    } else {
+      set_status(v.status + p, DOCP_DIMENSION, DOCP_AT_INITIAL_GUESS, 0);
+    }
+  }
+}
+
+/// Next active list: problems still OK and not converged (order is
+/// irrelevant: problems are independent).
+__global__ void compact_kernel(View v, const int* __restrict__ in, const int* __restrict__ n_in,
+                               int* __restrict__ out, int* __restrict__ n_out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < *n_in; k += gridDim.x * blockDim.x) {
+    const int p = in[k];
+    if (v.status[p].code == DOCP_OK && !v.converged[p]) out[atomicAdd(n_out, 1)] = p;
+  }
+}
+
+/// Problems whose status is OK (the finalize / backward set).
+__global__ void ok_list_kernel(View v, int* __restrict__ out, int* __restrict__ n_out) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < v.B; p += gridDim.x * blockDim.x)
+    if (v.status[p].code == DOCP_OK) out[atomicAdd(n_out, 1)] = p;
+}
+
+__global__ void iota_kernel(int* out, int n, int* count) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) out[k] = k;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = n;
+}
+
+__global__ void reset_status_kernel(View v) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < v.B; p += gridDim.x * blockDim.x)
+    set_status(v.status + p, DOCP_OK, DOCP_AT_NONE, 0);
+}
+
+// ---------------------------------------------------------------- launch helpers
+int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur) {
+  const int sp = std::max(b->d.bsz, b->d.nx * b->d.nu);
+  const size_t smem = static_cast<size_t>(kAsmWarps) * 6 * sp * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  const int grid = std::max(1, std::min(n_hint, b->num_sms * 8));
+  assemble_kernel<<<grid, kAsmThreads, smem, b->stream>>>(b->v, list, count, eps_pd, do_schur);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+int launch_gamma(docp_batch* b, const int* list, const int* count, int n_hint, int rhs) {
+  gamma_kernel<<<grid_for(static_cast<long>(n_hint) * b->d.nl, 256, b->num_sms * 16), 256, 0, b->stream>>>(
+      b->v, list, count, rhs);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+int launch_recover(docp_batch* b, const int* list, const int* count, int n_hint, const double* lam, int rhs) {
+  recover_kernel<<<grid_for(static_cast<long>(n_hint) * b->d.nz, 256, b->num_sms * 16), 256, 0, b->stream>>>(
+      b->v, list, count, lam, rhs);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+// ---- PCG variant selection
+struct PcgPlan {
+  bool resident;
+  int threads;
+  int maxr;
+  size_t smem;
+};
+
+size_t pcg_smem(const Dims& d, bool resident, bool parity) {
+  auto up2 = [](long n) { return (n + 1) & ~1L; };
+  long dbl = 2 * up2(d.nl) + 64;
+  if (parity) dbl += up2(d.nl) + up2(d.nb);
+  if (resident) dbl += d.blk_stride;
+  return static_cast<size_t>(dbl) * sizeof(double);
+}
+
+PcgPlan plan_pcg(const docp_batch* b, bool parity) {
+  PcgPlan pl{};
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device);
+  const size_t static_smem = 64;
+  pl.resident = pcg_smem(b->d, true, parity) + static_smem <= static_cast<size_t>(max_optin);
+  pl.smem = pcg_smem(b->d, pl.resident, parity);
+  const int nl = b->d.nl;
+  pl.threads = std::min(kPcgMaxThreads, (nl + 31) / 32 * 32);
+  const int need = (nl + pl.threads - 1) / pl.threads;
+  pl.maxr = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : 0;
+  return pl;
+}
+
+template <int NX, int MAXR, bool PAR, bool RES>
+int launch_pcg_t(docp_batch* b, const PcgPlan& pl, const int* list, const int* count, int n_hint, double* sol,
+                 double eps, int max_iters) {
+  auto kern = pcg_kernel<NX, MAXR, PAR, RES>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl.threads, pl.smem));
+  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit on an SM (smem %zu)", pl.smem);
+  const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
+  CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
+  kern<<<grid, pl.threads, pl.smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+template <int NX, bool PAR, bool RES>
+int launch_pcg_r(docp_batch* b, const PcgPlan& pl, const int* list, const int* count, int n_hint, double* sol,
+                 double eps, int max_iters) {
+  switch (pl.maxr) {
+    case 1: return launch_pcg_t<NX, 1, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
+    case 2: return launch_pcg_t<NX, 2, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
+    case 4: return launch_pcg_t<NX, 4, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
+    case 8: return launch_pcg_t<NX, 8, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
+    default: return fail(DOCP_UNSUPPORTED, "pcg: system dimension %d too large", b->d.nl);
+  }
+}
+
+template <int NX>
+int launch_pcg_nx(docp_batch* b, const PcgPlan& pl, bool par, const int* list, const int* count, int n_hint,
+                  double* sol, double eps, int max_iters) {
+  if (par) {
+    return pl.resident ? launch_pcg_r<NX, true, true>(b, pl, list, count, n_hint, sol, eps, max_iters)
+                       : launch_pcg_r<NX, true, false>(b, pl, list, count, n_hint, sol, eps, max_iters);
+  }
+  return pl.resident ? launch_pcg_r<NX, false, true>(b, pl, list, count, n_hint, sol, eps, max_iters)
+                     : launch_pcg_r<NX, false, false>(b, pl, list, count, n_hint, sol, eps, max_iters);
+}
+
+int launch_pcg(docp_batch* b, const docp_pcg_config& cfg, const int* list, const int* count, int n_hint,
+               double* sol) {
+  if (!(cfg.epsilon > 0.0 && cfg.max_iters >= 0)) return fail(DOCP_DIMENSION, "pcg: invalid config");
+  const bool par = cfg.mode == DOCP_PCG_PARITY;
+  const PcgPlan pl = plan_pcg(b, par);
+  g_pcg_invocations.fetch_add(static_cast<uint64_t>(n_hint), std::memory_order_relaxed);
+  switch (b->d.nx) {
+    case 4: return launch_pcg_nx<4>(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+    case 8: return launch_pcg_nx<8>(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+    default: return launch_pcg_nx<0>(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+  }
+}
+
+int launch_step(docp_batch* b, const docp_sqp_config& cfg, const int* list, const int* count, int n_hint, int iter,
+                int is_loop) {
+  StepCfg sc{};
+  sc.n_alpha = cfg.n_step_candidates;
+  for (int i = 0; i < sc.n_alpha; ++i) sc.alphas[i] = cfg.step_candidates[i];
+  sc.eta_armijo = cfg.eta_armijo;
+  sc.rho_penalty = cfg.rho_penalty;
+  sc.mu_floor = cfg.mu_floor_denominator;
+  sc.conv_tol = cfg.convergence_tol;
+  sc.iter = iter;
+  sc.max_iters = cfg.max_sqp_iters;
+  sc.is_loop = is_loop;
+  const int T = b->d.T;
+  const size_t smem = (static_cast<size_t>(sc.n_alpha + 1) * (3 * T + 2) + 2 * (2 * T + 1)) * sizeof(double);
+  CUDA_TRY(cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  if (smem > 200 * 1024) return fail(DOCP_UNSUPPORTED, "line search: horizon too long");
+  const int grid = std::max(1, std::min(n_hint, b->num_sms * 8));
+  step_kernel<<<grid, kStepThreads, smem, b->stream>>>(b->v, list, count, sc);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+int launch_kkt(docp_batch* b, const int* list, const int* count, int n_hint) {
+  kkt_kernel<<<std::max(1, std::min(n_hint, b->num_sms * 8)), 64, 0, b->stream>>>(b->v, list, count);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+int read_count(docp_batch* b, const int* dev_count, int* out) {
+  CUDA_TRY(cudaMemcpyAsync(b->h_count, dev_count, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  *out = *b->h_count;
+  return DOCP_OK;
+}
+
+int validate_sqp(const docp_sqp_config* cfg) {  // sqp.hpp:23-33
+  if (!cfg) return fail(DOCP_INVALID, "null config");
+  if (cfg->n_step_candidates < 1) return fail(DOCP_DIMENSION, "sqp: empty step candidate list");
+  if (cfg->n_step_candidates > DOCP_MAX_STEP_CANDIDATES)
+    return fail(DOCP_UNSUPPORTED, "sqp: at most %d step candidates", DOCP_MAX_STEP_CANDIDATES);
+  for (int i = 0; i < cfg->n_step_candidates; ++i) {
+    const double a = cfg->step_candidates[i];
+    const bool in_range = a > 0.0 && a <= 1.0;
+    const bool decreasing = i == 0 || a < cfg->step_candidates[i - 1];
+    if (!(in_range && decreasing))
+      return fail(DOCP_DIMENSION, "sqp: step candidates must be strictly decreasing in (0,1]");
+  }
+  if (!(cfg->eta_armijo > 0.0 && cfg->eta_armijo < 1.0)) return fail(DOCP_DIMENSION, "sqp: eta out of range");
+  return DOCP_OK;
+}
+
+double* field_base(docp_batch* b, int f, size_t* per, size_t* elem) {
+  const Dims& d = b->d;
+  *elem = sizeof(double);
+  switch (f) {
+    case DOCP_F_THETA: *per = d.nth; return b->v.theta;
+    case DOCP_F_Z: *per = d.nz; return b->v.z;
+    case DOCP_F_LAMBDA: *per = d.nl; return b->v.lam;
+    case DOCP_F_LAMBDA_TILDE: *per = d.nl; return b->v.lt;
+    case DOCP_F_LOSS_GRAD_Z: *per = d.nz; return b->v.lgz;
+    case DOCP_F_GRAD_THETA: *per = d.nth; return b->v.grad;
+    case DOCP_F_GAMMA: *per = d.nl; return b->v.gamma;
+    case DOCP_F_Z_QP: *per = d.nz; return b->v.zqp;
+    case DOCP_F_KKT: *per = 1; return b->v.kkt;
+    case DOCP_F_FINAL_ETA: *per = 1; return b->v.final_eta;
+    case DOCP_F_STEP_SIZES: *per = b->max_hist; return b->v.step_sizes;
+    case DOCP_F_MU: *per = 1; return b->v.mu;
+    case DOCP_F_ALPHA: *per = 1; return b->v.alpha;
+    case DOCP_F_LOSS: *per = 1; return b->v.loss;
+    default: break;
+  }
+  *elem = sizeof(int);
+  switch (f) {
+    case DOCP_F_STATUS: *per = 1; *elem = sizeof(docp_status); return reinterpret_cast<double*>(b->v.status);
+    case DOCP_F_SQP_ITERS: *per = 1; return reinterpret_cast<double*>(b->v.sqp_iters);
+    case DOCP_F_CONVERGED: *per = 1; return reinterpret_cast<double*>(b->v.converged);
+    case DOCP_F_PCG_ITERS: *per = 1; return reinterpret_cast<double*>(b->v.pcg_iters);
+    case DOCP_F_PCG_CONVERGED: *per = 1; return reinterpret_cast<double*>(b->v.pcg_conv);
+    case DOCP_F_PCG_HISTORY: *per = b->max_hist; return reinterpret_cast<double*>(b->v.pcg_hist);
+    case DOCP_F_PD_PROJECTED: *per = 1; return reinterpret_cast<double*>(b->v.pd_proj);
+    case DOCP_F_ACCEPTED: *per = 1; return reinterpret_cast<double*>(b->v.accepted);
+    default: return nullptr;
+  }
+}
+
+int check_problem(const docp_problem* p) {
+  if (!p) return fail(DOCP_INVALID, "null problem");
+  if (p->family != DOCP_AFFINE_QUADRATIC && p->family != DOCP_CARTPOLE)
+    return fail(DOCP_UNSUPPORTED, "unknown problem family %d", p->family);
+  if (p->n_x < 1 || p->n_u < 1 || p->horizon < 1) return fail(DOCP_DIMENSION, "dimensions must be positive");
+  if (p->n_x > kMaxNx || p->n_u > kMaxNu)
+    return fail(DOCP_UNSUPPORTED, "n_x, n_u must be <= %d (got %d, %d)", kMaxNx, p->n_x, p->n_u);
+  if (p->family == DOCP_CARTPOLE && (p->n_x != 4 || p->n_u != 1))
+    return fail(DOCP_DIMENSION, "cart-pole has n_x = 4, n_u = 1");
+  return DOCP_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+int docp_abi_version(void) { return DOCP_ABI_VERSION; }
+
+int docp_theta_size(const docp_problem* p) {
+  if (check_problem(p)) return -1;
+  return make_dims(*p).nth;
+}
+
+int docp_batch_create(const docp_problem* problem, int32_t batch_size, int32_t device, docp_batch** out) {
+  if (!out) return fail(DOCP_INVALID, "null out");
+  *out = nullptr;
+  int rc = check_problem(problem);
+  if (rc) return rc;
+  if (batch_size < 1) return fail(DOCP_DIMENSION, "batch size must be >= 1");
+  CUDA_TRY(cudaSetDevice(device));
+  auto* b = new docp_batch;
+  b->prob = *problem;
+  b->d = make_dims(*problem);
+  b->B = batch_size;
+  b->device = device;
+  cudaDeviceGetAttribute(&b->num_sms, cudaDevAttrMultiProcessorCount, device);
+  const Dims& d = b->d;
+  const size_t B = static_cast<size_t>(batch_size);
+  View& v = b->v;
+  v.d = d;
+  v.B = batch_size;
+  v.prob = *problem;
+#define A(ptr, n)                                  \
+  if ((rc = dalloc(b, &ptr, (n)))) {               \
+    delete b;                                      \
+    return rc;                                     \
+  }
+  A(v.theta, B * d.nth);
+  A(v.z, B * d.nz);
+  A(v.lam, B * d.nl);
+  A(v.lt, B * d.nl);
+  A(v.lgz, B * d.nz);
+  A(v.grad, B * d.nth);
+  A(v.gamma, B * d.nl);
+  A(v.zqp, B * d.nz);
+  A(v.qd, B * d.nb * d.nx);
+  A(v.lq, B * d.nb * d.nx);
+  A(v.q, B * d.nb * d.nx);
+  A(v.rd, B * d.T * d.nu);
+  A(v.lr, B * d.T * d.nu);
+  A(v.r, B * d.T * d.nu);
+  A(v.A, B * d.T * d.bsz);
+  A(v.Bm, B * d.T * d.nx * d.nu);
+  A(v.C, B * d.T * d.nx);
+  A(v.xs, B * d.nx);
+  A(v.blocks, B * d.blk_stride);
+  A(v.status, B);
+  A(v.sqp_iters, B);
+  A(v.converged, B);
+  A(v.pcg_iters, B);
+  A(v.pcg_conv, B);
+  A(v.pd_proj, B);
+  A(v.accepted, B);
+  A(v.kkt, B);
+  A(v.final_eta, B);
+  A(v.mu, B);
+  A(v.alpha, B);
+  A(v.loss, B);
+  A(b->all_list, B);
+  A(b->list[0], B);
+  A(b->list[1], B);
+  A(b->counts, 8);
+#undef A
+  if ((rc = ensure_hist(b, 20))) {
+    delete b;
+    return rc;
+  }
+  if (cudaMallocHost(&b->h_count, sizeof(int)) != cudaSuccess) {
+    delete b;
+    return fail(DOCP_CUDA_ERROR, "cudaMallocHost failed");
+  }
+  iota_kernel<<<grid_for(batch_size, 256, 4096), 256, 0, b->stream>>>(b->all_list, batch_size, b->counts);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(b->stream) != cudaSuccess) {
+    delete b;
+    return fail(DOCP_CUDA_ERROR, "batch init failed");
+  }
+  *out = b;
+  return DOCP_OK;
+}
+
+void docp_batch_destroy(docp_batch* b) { delete b; }
+
+int docp_batch_set_stream(docp_batch* b, void* stream) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  b->stream = static_cast<cudaStream_t>(stream);
+  return DOCP_OK;
+}
+
+int docp_batch_sync(docp_batch* b) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  return DOCP_OK;
+}
+
+int32_t docp_batch_size(const docp_batch* b) { return b ? b->B : 0; }
+
+int docp_batch_field_ptr(docp_batch* b, int32_t field, void** ptr, size_t* bytes) {
+  if (!b || !ptr) return fail(DOCP_INVALID, "null argument");
+  size_t per = 0, elem = 0;
+  double* base = field_base(b, field, &per, &elem);
+  if (!base) return fail(DOCP_INVALID, "unknown field %d", field);
+  *ptr = base;
+  if (bytes) *bytes = per * elem * static_cast<size_t>(b->B);
+  return DOCP_OK;
+}
+
+int docp_batch_upload(docp_batch* b, int32_t field, const void* src, int32_t on_device) {
+  void* dst;
+  size_t bytes;
+  int rc = docp_batch_field_ptr(b, field, &dst, &bytes);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, b->stream));
+  if (!on_device) CUDA_TRY(cudaStreamSynchronize(b->stream));
+  return DOCP_OK;
+}
+
+int docp_batch_download(docp_batch* b, int32_t field, void* dst, int32_t on_device) {
+  void* src;
+  size_t bytes;
+  int rc = docp_batch_field_ptr(b, field, &src, &bytes);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, b->stream));
+  if (!on_device) CUDA_TRY(cudaStreamSynchronize(b->stream));
+  return DOCP_OK;
+}
+
+int docp_batch_upload_schur(docp_batch* b, const double* s_diag, const double* s_sub, const double* p_diag,
+                            const double* p_super) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  const Dims& d = b->d;
+  const int nx = d.nx;
+  std::vector<double> rec(static_cast<size_t>(b->B) * d.blk_stride, 0.0);
+  for (int p = 0; p < b->B; ++p) {
+    double* r = rec.data() + static_cast<size_t>(p) * d.blk_stride;
+    auto put = [&](const double* src, long region, int nblk) {
+      for (int k = 0; k < nblk; ++k)
+        for (int s = 0; s < nx; ++s)
+          for (int e = 0; e < nx; ++e)
+            r[region + static_cast<long>(k) * d.bsz + blk_off(nx, k, e, s)] =
+                src[(static_cast<size_t>(p) * nblk + k) * d.bsz + e + s * nx];
+    };
+    put(s_diag, d.s_diag, d.nb);
+    put(s_sub, d.s_sub, d.T);
+    put(p_diag, d.p_diag, d.nb);
+    put(p_super, d.p_sup, d.T);
+  }
+  CUDA_TRY(cudaMemcpyAsync(b->v.blocks, rec.data(), rec.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  return DOCP_OK;
+}
+
+int docp_batch_download_schur(docp_batch* b, double* s_diag, double* s_sub, double* p_diag, double* p_super) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  const Dims& d = b->d;
+  const int nx = d.nx;
+  std::vector<double> rec(static_cast<size_t>(b->B) * d.blk_stride);
+  CUDA_TRY(cudaMemcpyAsync(rec.data(), b->v.blocks, rec.size() * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  for (int p = 0; p < b->B; ++p) {
+    const double* r = rec.data() + static_cast<size_t>(p) * d.blk_stride;
+    auto get = [&](double* dst, long region, int nblk) {
+      if (!dst) return;
+      for (int k = 0; k < nblk; ++k)
+        for (int s = 0; s < nx; ++s)
+          for (int e = 0; e < nx; ++e)
+            dst[(static_cast<size_t>(p) * nblk + k) * d.bsz + e + s * nx] =
+                r[region + static_cast<long>(k) * d.bsz + blk_off(nx, k, e, s)];
+    };
+    get(s_diag, d.s_diag, d.nb);
+    get(s_sub, d.s_sub, d.T);
+    get(p_diag, d.p_diag, d.nb);
+    get(p_super, d.p_sup, d.T);
+  }
+  return DOCP_OK;
+}
+
+int docp_batch_download_qp(docp_batch* b, double* Q, double* q, double* R, double* r, double* A, double* Bm,
+                           double* C, double* x_s) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  const Dims& d = b->d;
+  const size_t B = static_cast<size_t>(b->B);
+  auto fetch = [&](const double* src, size_t n, std::vector<double>& out) -> int {
+    out.resize(n);
+    CUDA_TRY(cudaMemcpy(out.data(), src, n * sizeof(double), cudaMemcpyDeviceToHost));
+    return DOCP_OK;
+  };
+  std::vector<double> qd, rd, tmp;
+  int rc;
+  if ((rc = fetch(b->v.qd, B * d.nb * d.nx, qd)) || (rc = fetch(b->v.rd, B * d.T * d.nu, rd))) return rc;
+  if (Q) {
+    std::fill(Q, Q + B * d.nb * d.bsz, 0.0);
+    for (size_t k = 0; k < B * d.nb; ++k)
+      for (int i = 0; i < d.nx; ++i) Q[k * d.bsz + i + i * d.nx] = qd[k * d.nx + i];
+  }
+  if (R) {
+    const size_t b2 = static_cast<size_t>(d.nu) * d.nu;
+    std::fill(R, R + B * d.T * b2, 0.0);
+    for (size_t k = 0; k < B * d.T; ++k)
+      for (int i = 0; i < d.nu; ++i) R[k * b2 + i + i * d.nu] = rd[k * d.nu + i];
+  }
+  auto copy = [&](double* dst, const double* src, size_t n) -> int {
+    if (dst) CUDA_TRY(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost));
+    return DOCP_OK;
+  };
+  if ((rc = copy(q, b->v.q, B * d.nb * d.nx)) || (rc = copy(r, b->v.r, B * d.T * d.nu)) ||
+      (rc = copy(A, b->v.A, B * d.T * d.bsz)) || (rc = copy(Bm, b->v.Bm, B * d.T * d.nx * d.nu)) ||
+      (rc = copy(C, b->v.C, B * d.T * d.nx)) || (rc = copy(x_s, b->v.xs, B * d.nx)))
+    return rc;
+  return DOCP_OK;
+}
+
+// ---------------------------------------------------------------- primitives
+int docp_linearize(docp_batch* b, double eps_pd) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  b->last_eps_pd = eps_pd;
+  return launch_assemble(b, b->all_list, b->counts, b->B, eps_pd, 0);
+}
+
+int docp_assemble_schur(docp_batch* b) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  // The kernel rebuilds the (deterministic) QP data at the last
+  // linearization point (Z, THETA, eps_pd) and assembles from it.
+  return launch_assemble(b, b->all_list, b->counts, b->B, b->last_eps_pd, 1);
+}
+
+int docp_assemble_gamma(docp_batch* b, int32_t rhs) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  if (rhs != DOCP_RHS_FORWARD && rhs != DOCP_RHS_ADJOINT) return fail(DOCP_INVALID, "bad rhs");
+  return launch_gamma(b, b->all_list, b->counts, b->B, rhs);
+}
+
+int docp_pcg_solve(docp_batch* b, const docp_pcg_config* cfg, int32_t field) {
+  if (!b || !cfg) return fail(DOCP_INVALID, "null argument");
+  double* sol = field == DOCP_F_LAMBDA ? b->v.lam : field == DOCP_F_LAMBDA_TILDE ? b->v.lt : nullptr;
+  if (!sol) return fail(DOCP_INVALID, "pcg solution field must be LAMBDA or LAMBDA_TILDE");
+  reset_status_kernel<<<grid_for(b->B, 256, 4096), 256, 0, b->stream>>>(b->v);
+  LAUNCH_CHECK();
+  return launch_pcg(b, *cfg, b->all_list, b->counts, b->B, sol);
+}
+
+int docp_recover_primal(docp_batch* b, int32_t field, int32_t rhs) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  const double* lam = field == DOCP_F_LAMBDA ? b->v.lam : field == DOCP_F_LAMBDA_TILDE ? b->v.lt : nullptr;
+  if (!lam) return fail(DOCP_INVALID, "lambda field must be LAMBDA or LAMBDA_TILDE");
+  return launch_recover(b, b->all_list, b->counts, b->B, lam, rhs);
+}
+
+int docp_line_search(docp_batch* b, const docp_sqp_config* cfg) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  int rc = validate_sqp(cfg);
+  if (rc) return rc;
+  return launch_step(b, *cfg, b->all_list, b->counts, b->B, 0, 0);
+}
+
+int docp_kkt_residual(docp_batch* b) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  return launch_kkt(b, b->all_list, b->counts, b->B);
+}
+
+int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-261
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  int rc = validate_sqp(cfg);
+  if (rc) return rc;
+  if ((rc = ensure_hist(b, std::max(1, cfg->max_sqp_iters)))) return rc;
+  int cur = 0;
+  CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, 2 * sizeof(int), b->stream));
+  init_solve_kernel<<<grid_for(b->B, 128, 4096), 128, 0, b->stream>>>(b->v, b->list[0], b->counts + 1);
+  LAUNCH_CHECK();
+  int n_active = 0;
+  if ((rc = read_count(b, b->counts + 1, &n_active))) return rc;
+  for (int iter = 0; iter < cfg->max_sqp_iters && n_active > 0; ++iter) {
+    const int* list = b->list[cur];
+    const int* cnt = b->counts + 1 + cur;
+    if ((rc = launch_assemble(b, list, cnt, n_active, cfg->eps_pd, 1))) return rc;
+    if ((rc = launch_gamma(b, list, cnt, n_active, DOCP_RHS_FORWARD))) return rc;
+    if ((rc = launch_pcg(b, cfg->pcg, list, cnt, n_active, b->v.lam))) return rc;
+    if ((rc = launch_recover(b, list, cnt, n_active, b->v.lam, DOCP_RHS_FORWARD))) return rc;
+    if ((rc = launch_step(b, *cfg, list, cnt, n_active, iter, 1))) return rc;
+    const int nxt = cur ^ 1;
+    CUDA_TRY(cudaMemsetAsync(b->counts + 1 + nxt, 0, sizeof(int), b->stream));
+    compact_kernel<<<grid_for(n_active, 256, 4096), 256, 0, b->stream>>>(b->v, list, cnt, b->list[nxt],
+                                                                          b->counts + 1 + nxt);
+    LAUNCH_CHECK();
+    cur = nxt;
+    if ((rc = read_count(b, b->counts + 1 + cur, &n_active))) return rc;
+  }
+  // refresh QP / Schur at the returned trajectory, KKT diagnostic (sqp.hpp:254-259)
+  CUDA_TRY(cudaMemsetAsync(b->counts + 1 + (cur ^ 1), 0, sizeof(int), b->stream));
+  int* fin = b->list[cur ^ 1];
+  int* fin_cnt = b->counts + 1 + (cur ^ 1);
+  ok_list_kernel<<<grid_for(b->B, 256, 4096), 256, 0, b->stream>>>(b->v, fin, fin_cnt);
+  LAUNCH_CHECK();
+  if ((rc = launch_assemble(b, fin, fin_cnt, b->B, cfg->eps_pd, 1))) return rc;
+  if ((rc = launch_kkt(b, fin, fin_cnt, b->B))) return rc;
+  return DOCP_OK;
+}
+
+int docp_backward_vjp(docp_batch* b, const docp_pcg_config* cfg) {  // backward.hpp:27-50
+  if (!b || !cfg) return fail(DOCP_INVALID, "null argument");
+  int rc;
+  CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, sizeof(int), b->stream));
+  ok_list_kernel<<<grid_for(b->B, 256, 4096), 256, 0, b->stream>>>(b->v, b->list[0], b->counts + 1);
+  LAUNCH_CHECK();
+  const int* list = b->list[0];
+  const int* cnt = b->counts + 1;
+  if ((rc = launch_gamma(b, list, cnt, b->B, DOCP_RHS_ADJOINT))) return rc;
+  if ((rc = launch_pcg(b, *cfg, list, cnt, b->B, b->v.lt))) return rc;
+  if ((rc = launch_recover(b, list, cnt, b->B, b->v.lt, DOCP_RHS_ADJOINT))) return rc;
+  vjp_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 128, b->num_sms * 16), 128, 0, b->stream>>>(b->v, list,
+                                                                                                        cnt);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weights, int32_t learn_start,
+                  int32_t learn_size, const double* demos, double den, double* loss_sum, double* grad_sum) {
+  if (!b || !cfg || !weights || !demos || !loss_sum || !grad_sum) return fail(DOCP_INVALID, "null argument");
+  if (learn_start < 0 || learn_size < 0 || learn_start + learn_size > b->d.nth)
+    return fail(DOCP_DIMENSION, "learnable segment out of range");
+  int rc;
+  il_setup_kernel<<<grid_for(static_cast<long>(b->B) * (learn_size + b->d.nz), 256, b->num_sms * 16), 256, 0,
+                    b->stream>>>(b->v, weights, learn_start, learn_size, demos);
+  LAUNCH_CHECK();
+  if ((rc = docp_sqp_solve(b, cfg))) return rc;
+  il_loss_kernel<<<grid_for(b->B, 128, 4096), 128, 0, b->stream>>>(b->v, demos, den);
+  LAUNCH_CHECK();
+  if ((rc = docp_backward_vjp(b, &cfg->pcg))) return rc;
+  il_sum_kernel<<<grid_for(learn_size + 1, 64, 64), 64, 0, b->stream>>>(b->v, learn_start, learn_size, loss_sum,
+                                                                         grad_sum);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+uint64_t docp_pcg_invocations(void) { return g_pcg_invocations.load(); }
+uint64_t docp_kernel_launches(void) { return g_launches.load(); }
+const char* docp_last_error(void) { return g_last_error.c_str(); }
+
+int docp_format_status(const docp_status* s, char* buf, int32_t cap) {
+  if (!s || !buf || cap <= 0) return 0;
+  const int i = s->index;
+  switch (s->where) {  // messages of common.hpp / problem.hpp / schur.hpp / pcg.hpp / sqp.hpp
+    case DOCP_AT_NONE: return snprintf(buf, cap, "ok");
+    case DOCP_AT_STATE_COST: return snprintf(buf, cap, "state_cost returned non-finite values at stage %d", i);
+    case DOCP_AT_CONTROL_COST: return snprintf(buf, cap, "control_cost returned non-finite values at stage %d", i);
+    case DOCP_AT_DYNAMICS: return snprintf(buf, cap, "dynamics_residual returned non-finite values at stage %d", i);
+    case DOCP_AT_INITIAL_STATE: return snprintf(buf, cap, "initial_state returned non-finite values at stage %d", i);
+    case DOCP_AT_CHOL_Q: return snprintf(buf, cap, "assemble_schur: Cholesky of Q failed at stage %d", i);
+    case DOCP_AT_CHOL_R: return snprintf(buf, cap, "assemble_schur: Cholesky of R failed at stage %d", i);
+    case DOCP_AT_CHOL_CHI: return snprintf(buf, cap, "assemble_schur: Cholesky of chi failed at stage %d", i);
+    case DOCP_AT_PCG_CURVATURE:
+      return snprintf(buf, cap, "pcg: p'Sp <= 0 (loss of positive definiteness) at iteration %d", i);
+    case DOCP_AT_PCG_PRECOND: return snprintf(buf, cap, "pcg: preconditioner lost definiteness at iteration %d", i);
+    case DOCP_AT_MERIT_STATE: return snprintf(buf, cap, "merit: non-finite state cost at stage %d", i);
+    case DOCP_AT_MERIT_CONTROL: return snprintf(buf, cap, "merit: non-finite control cost at stage %d", i);
+    case DOCP_AT_SQP_ITERATE: return snprintf(buf, cap, "sqp: non-finite iterate at iteration %d", i);
+    case DOCP_AT_INITIAL_GUESS: return snprintf(buf, cap, "sqp: initial guess must be finite");
+    default: return snprintf(buf, cap, "error %d at %d", s->code, i);
+  }
+}
+
+int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
+  if (check_problem(p) || !buf) return -1;
+  const Dims d = make_dims(*p);
+  int dev = 0, max_optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const bool res = pcg_smem(d, true, false) + 64 <= static_cast<size_t>(max_optin);
+  return snprintf(buf, cap, "nx=%d layout=%s pcg=%s record=%ld B", d.nx,
+                  d.nx == 8 ? "swizzle8" : d.nx == 4 ? "swizzle4" : "colmajor", res ? "resident(TMA)" : "streaming",
+                  d.blk_stride * 8);
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+// families.cuh — device problem families (the OcpDefinition callbacks of
+// the reference, which cannot cross to the GPU as std::function).
+//
+// Every expression keeps the reference's evaluation order so that, compiled
+// with --fmad=false, stage values are bit-identical to the reference headers
+// (cart-pole's sin/cos aside: CUDA's are within 2 ulp of glibc's).
+#pragma once
+
+#include "common.cuh"
+
+namespace docp_dev {
+
+/// Diagonal quadratic stage cost  scale * v' diag(w) v
+/// (affine_quadratic.hpp:47-64, quadratic_cost.hpp:9-20). Returns the value;
+/// grad_i = ((2 scale) w_i) v_i and hess = diag((2 scale) w_i).
+__device__ inline double diag_cost_value(double scale, const double* w, const double* v, int n) {
+  double acc = v[0] * (w[0] * v[0]);
+  for (int i = 1; i < n; ++i) acc = acc + v[i] * (w[i] * v[i]);
+  return scale * acc;
+}
+__device__ inline double diag_cost_grad(double scale, double w, double v) { return ((2.0 * scale) * w) * v; }
+__device__ inline double diag_cost_hess(double scale, double w) { return (2.0 * scale) * w; }
+
+struct Family {
+  int kind;
+  double scale;
+  double cart_mass, pole_mass, length, gravity, dt;
+
+  __host__ __device__ static Family from(const docp_problem& p) {
+    Family f;
+    f.kind = p.family;
+    f.scale = p.family == DOCP_CARTPOLE ? 0.5 : p.cost_scale;
+    f.cart_mass = p.cart_mass;
+    f.pole_mass = p.pole_mass;
+    f.length = p.length;
+    f.gravity = p.gravity;
+    f.dt = p.dt;
+    return f;
+  }
+
+  __device__ const double* w_x(const Dims&, const double* th) const { return th; }
+  __device__ const double* w_u(const Dims& d, const double* th) const { return th + d.nx; }
+  /// initial_state(theta)
+  __device__ const double* x_s(const Dims& d, const double* th) const {
+    if (kind == DOCP_CARTPOLE) return th + 5;
+    return th + d.nx + d.nu + d.nx * d.nx + d.nx * d.nu + d.nx;
+  }
+
+  /// Dynamics residual f = x+ - phi(x, u) and its Jacobians (jac_x_next = I).
+  /// res[nx]; jx[nx*nx], ju[nx*nu] column-major (may be null).
+  __device__ void dynamics(const Dims& d, const double* th, const double* xn, const double* x, const double* u,
+                           double* res, double* jx, double* ju) const {
+    const int nx = d.nx, nu = d.nu;
+    if (kind == DOCP_AFFINE_QUADRATIC) {  // affine_quadratic.hpp:65-75
+      const double* a = th + nx + nu;
+      const double* b = a + nx * nx;
+      const double* off = b + nx * nu;
+      for (int i = 0; i < nx; ++i) {
+        double ax = a[i] * x[0];
+        for (int k = 1; k < nx; ++k) ax = ax + a[i + k * nx] * x[k];
+        double bu = b[i] * u[0];
+        for (int k = 1; k < nu; ++k) bu = bu + b[i + k * nx] * u[k];
+        res[i] = ((xn[i] - ax) - bu) - off[i];
+      }
+      if (jx)
+        for (int k = 0; k < nx * nx; ++k) jx[k] = -a[k];
+      if (ju)
+        for (int k = 0; k < nx * nu; ++k) ju[k] = -b[k];
+      return;
+    }
+    // cart-pole: make_explicit_dynamics(cartpole_step), cartpole.hpp:28-78
+    const double sn = sin(x[2]);
+    const double c = cos(x[2]);
+    const double mp = pole_mass;
+    const double len = length;
+    const double g = gravity;
+    const double big_m = cart_mass + pole_mass;
+    const double dd = big_m + mp * (1.0 - c * c);
+    const double xd1 = (-mp * len * sn * x[3] * x[3] + mp * g * sn * c) / (dd * len);
+    const double xd3 = (-mp * len * sn * x[3] + mp * g * sn * c + u[0]) / dd;
+    res[0] = xn[0] - (x[0] + dt * x[1]);
+    res[1] = xn[1] - (x[1] + dt * xd1);
+    res[2] = xn[2] - (x[2] + dt * x[3]);
+    res[3] = xn[3] - (x[3] + dt * xd3);
+    if (jx) {
+      const double d_d3 = 2.0 * mp * sn * c;
+      const double n2 = -mp * len * sn * x[3] * x[3] + mp * g * sn * c;
+      const double n2_d3 = -mp * len * c * x[3] * x[3] + mp * g * (c * c - sn * sn);
+      const double n2_d4 = -2.0 * mp * len * sn * x[3];
+      const double n4 = -mp * len * sn * x[3] + mp * g * sn * c + u[0];
+      const double n4_d3 = -mp * len * c * x[3] + mp * g * (c * c - sn * sn);
+      const double n4_d4 = -mp * len * sn;
+      double J[16];
+      for (int k = 0; k < 16; ++k) J[k] = 0.0;
+      J[0 + 1 * 4] = 1.0;
+      J[1 + 2 * 4] = (n2_d3 * dd - n2 * d_d3) / (dd * dd * len);
+      J[1 + 3 * 4] = n2_d4 / (dd * len);
+      J[2 + 3 * 4] = 1.0;
+      J[3 + 2 * 4] = (n4_d3 * dd - n4 * d_d3) / (dd * dd);
+      J[3 + 3 * 4] = n4_d4 / dd;
+      for (int j = 0; j < 4; ++j)
+        for (int i = 0; i < 4; ++i) jx[i + j * 4] = -((i == j ? 1.0 : 0.0) + dt * J[i + j * 4]);
+    }
+    if (ju) {
+      ju[0] = -(dt * 0.0);
+      ju[1] = -(dt * 0.0);
+      ju[2] = -(dt * 0.0);
+      ju[3] = -(dt * (1.0 / dd));
+    }
+  }
+};
+
+}  // namespace docp_dev

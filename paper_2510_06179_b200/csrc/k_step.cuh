@@ -1,0 +1,398 @@
+// k_step.cuh — K3 (SQP merit + line search + convergence test), the KKT
+// diagnostic, K4's theta-VJP contraction and the imitation-learning epoch
+// helpers.
+//
+//   line_search + sqp loop body   sqp.hpp:151-206, 236-251
+//   merit_parts                   sqp.hpp:98-123
+//   kkt_residual                  problem.hpp:263-300
+//   theta_vjp                     affine_quadratic.hpp:82-117, quadratic_cost.hpp:24-45
+//   train_il epoch body           train.hpp:87-131
+//
+// Per-stage terms are evaluated in parallel (one thread per (candidate,
+// stage) task); every sum the reference accumulates is then folded by one
+// thread in the reference's order, so the line-search decision sees exactly
+// the reference's numbers.
+#pragma once
+
+#include "families.cuh"
+
+namespace docp_dev {
+
+constexpr int kStepThreads = 256;
+
+struct StepCfg {
+  int n_alpha;
+  double alphas[DOCP_MAX_STEP_CANDIDATES];
+  double eta_armijo, rho_penalty, mu_floor, conv_tol;
+  int iter;       // SQP iteration index (history slot)
+  int max_iters;  // cfg.max_sqp_iters
+  int is_loop;    // 1: sqp loop body (update counters/convergence); 0: bare line_search
+};
+
+/// Stage terms of merit_parts at one trajectory version (old or a trial).
+/// Slots: state value t -> t, control value t -> T+1+t, dynamics |res|_1
+/// t -> 2T+1+t, initial-condition |x_0 - x_s|_1 -> 3T+1.
+__device__ inline void merit_task(const Dims& d, const Family& fam, const double* th, const double* zo,
+                                  const double* zq, double alpha, bool trial, int task, double* slots) {
+  const int nx = d.nx, nu = d.nu, T = d.T;
+  double a[kMaxNx], b[kMaxNx], c[kMaxNx], res[kMaxNx];
+  auto get = [&](int off, int n, double* out) {
+    for (int i = 0; i < n; ++i)
+      out[i] = trial ? zo[off + i] + alpha * (zq[off + i] - zo[off + i]) : zo[off + i];
+  };
+  if (task <= T) {
+    get(xoff(d, task), nx, a);
+    slots[task] = diag_cost_value(fam.scale, fam.w_x(d, th), a, nx);
+  } else if (task < 2 * T + 1) {
+    const int t = task - (T + 1);
+    get(xoff(d, t), nx, a);
+    get(uoff(d, t), nu, b);
+    get(xoff(d, t + 1), nx, c);
+    slots[T + 1 + t] = diag_cost_value(fam.scale, fam.w_u(d, th), b, nu);
+    fam.dynamics(d, th, c, a, b, res, nullptr, nullptr);
+    double s = fabs(res[0]);
+    for (int i = 1; i < nx; ++i) s = s + fabs(res[i]);
+    slots[2 * T + 1 + t] = s;
+  } else {
+    get(xoff(d, 0), nx, a);
+    const double* x_s = fam.x_s(d, th);
+    double s = fabs(a[0] - x_s[0]);
+    for (int i = 1; i < nx; ++i) s = s + fabs(a[i] - x_s[i]);
+    slots[3 * T + 1] = s;
+  }
+}
+
+/// Folds one version's slots in merit_parts order; returns false (and the
+/// first failing slot) when a cost value is non-finite.
+__device__ inline bool merit_fold(const Dims& d, const double* slots, double* cost, double* viol, int* bad_slot) {
+  const int T = d.T;
+  double c = 0.0, v = 0.0;
+  for (int t = 0; t <= T; ++t) {
+    if (!isfinite(slots[t])) {
+      *bad_slot = t;
+      return false;
+    }
+    c = c + slots[t];
+  }
+  for (int t = 0; t < T; ++t) {
+    if (!isfinite(slots[T + 1 + t])) {
+      *bad_slot = T + 1 + t;
+      return false;
+    }
+    c = c + slots[T + 1 + t];
+    v = v + slots[2 * T + 1 + t];
+  }
+  v = v + slots[3 * T + 1];
+  *cost = c;
+  *viol = v;
+  return true;
+}
+
+/// K3: line search from Z toward Z_QP and the SQP-loop bookkeeping.
+__global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* __restrict__ work,
+                                                           const int* __restrict__ n_work, StepCfg cfg) {
+  extern __shared__ double sm_step[];
+  __shared__ double s_dc, s_cv, s_mu, s_alpha, s_step;
+  __shared__ double s_cost[DOCP_MAX_STEP_CANDIDATES + 1], s_viol[DOCP_MAX_STEP_CANDIDATES + 1];
+  __shared__ int s_bad[DOCP_MAX_STEP_CANDIDATES + 1];
+  __shared__ int s_nonfinite, s_accepted;
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, T = d.T;
+  const Family fam = Family::from(v.prob);
+  const int tid = threadIdx.x;
+  const int nslot = 3 * T + 2;
+  const int nver = cfg.n_alpha + 1;
+  double* slots = sm_step;                          // [nver][nslot]
+  double* dterm = slots + static_cast<long>(nver) * nslot;  // [2T+1] d_cost terms
+  double* cterm = dterm + 2 * T + 1;                 // [2T+1] curvature terms
+
+  for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
+    const int p = work[w];
+    if (v.status[p].code != DOCP_OK) continue;
+    const double* th = v.theta + static_cast<long>(p) * d.nth;
+    double* zo = v.z + static_cast<long>(p) * d.nz;
+    const double* zq = v.zqp + static_cast<long>(p) * d.nz;
+    const double* qd = v.qd + static_cast<long>(p) * d.nb * nx;
+    const double* rd = v.rd + static_cast<long>(p) * T * nu;
+
+    // d_cost and curvature stage terms (sqp.hpp:161-172): unprojected
+    // gradients at z_old, projected Q / R
+    for (int t = tid; t < 2 * T + 1; t += blockDim.x) {
+      const bool st = t <= T;
+      const int s = st ? t : t - (T + 1);
+      const int n = st ? nx : nu;
+      const int off = st ? xoff(d, s) : uoff(d, s);
+      const double* w = st ? fam.w_x(d, th) : fam.w_u(d, th);
+      const double* h = st ? qd + s * nx : rd + s * nu;
+      double dc = 0.0, cv = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double dx = zq[off + i] - zo[off + i];
+        const double g = diag_cost_grad(fam.scale, w[i], zo[off + i]);
+        const double qdx = h[i] * dx;
+        dc = i == 0 ? g * dx : dc + g * dx;
+        cv = i == 0 ? dx * qdx : cv + dx * qdx;
+      }
+      dterm[t] = dc;
+      cterm[t] = cv;
+    }
+    for (int task = tid; task < nver * (2 * T + 2); task += blockDim.x) {
+      const int ver = task / (2 * T + 2);
+      const int tt = task % (2 * T + 2);
+      merit_task(d, fam, th, zo, zq, ver == 0 ? 0.0 : cfg.alphas[ver - 1], ver > 0, tt,
+                 slots + static_cast<long>(ver) * nslot);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double dc = 0.0, cv = 0.0;
+      for (int t = 0; t < 2 * T + 1; ++t) {
+        dc = dc + dterm[t];
+        cv = cv + cterm[t];
+      }
+      s_dc = dc;
+      s_cv = cv;
+    } else if (tid - 1 < nver) {
+      const int ver = tid - 1;
+      double c = 0.0, vv = 0.0;
+      int bad = -1;
+      const bool ok = merit_fold(d, slots + static_cast<long>(ver) * nslot, &c, &vv, &bad);
+      s_cost[ver] = c;
+      s_viol[ver] = vv;
+      s_bad[ver] = ok ? -1 : bad;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int err_ver = -1;
+      for (int ver = 0; ver < nver; ++ver)
+        if (s_bad[ver] >= 0) {
+          err_ver = ver;
+          break;
+        }
+      if (err_ver >= 0) {
+        const int slot = s_bad[err_ver];
+        if (slot <= T) set_status(v.status + p, DOCP_EVALUATION, DOCP_AT_MERIT_STATE, slot);
+        else set_status(v.status + p, DOCP_EVALUATION, DOCP_AT_MERIT_CONTROL, slot - (T + 1));
+        s_alpha = -1.0;
+      } else {
+        // penalty rule (sqp.hpp:174-183)
+        const double viol = s_viol[0];
+        double mu = v.mu[p];
+        if (viol >= cfg.mu_floor) {
+          const double required = (s_dc + 0.5 * s_cv) / ((1.0 - cfg.rho_penalty) * viol);
+          if (isfinite(required) && required > mu) mu = required;
+        }
+        const double phi_old = s_cost[0] + mu * viol;
+        const double descent = s_dc - mu * viol;
+        double alpha = cfg.alphas[cfg.n_alpha - 1];
+        int acc = 0;
+        for (int c = 0; c < cfg.n_alpha; ++c) {
+          const double merit = s_cost[c + 1] + mu * s_viol[c + 1];
+          const double dphi = merit - phi_old - cfg.eta_armijo * cfg.alphas[c] * descent;
+          if (dphi < 0.0) {
+            alpha = cfg.alphas[c];
+            acc = 1;
+            break;
+          }
+        }
+        s_mu = mu;
+        s_alpha = alpha;
+        s_accepted = acc;
+      }
+      s_nonfinite = 0;
+      s_step = 0.0;
+    }
+    __syncthreads();
+    const double alpha = s_alpha;
+    if (alpha < 0.0) continue;  // merit evaluation failed
+    // z_new = z_old.interpolate(z_qp, alpha) and the step norm (trajectory.hpp:57-68)
+    double stepmax = 0.0;
+    for (int e = tid; e < d.nz; e += blockDim.x) {
+      const double zn = zo[e] + alpha * (zq[e] - zo[e]);
+      if (!isfinite(zn)) s_nonfinite = 1;
+      stepmax = fmax(stepmax, fabs(zn - zo[e]));
+    }
+    stepmax = warp_max(stepmax);
+    if ((tid & 31) == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_step), __double_as_longlong(stepmax));
+    __syncthreads();
+    const bool diverged = s_nonfinite != 0;
+    if (!diverged)
+      for (int e = tid; e < d.nz; e += blockDim.x) zo[e] = zo[e] + alpha * (zq[e] - zo[e]);
+    if (tid == 0) {
+      v.mu[p] = s_mu;
+      v.alpha[p] = alpha;
+      v.accepted[p] = s_accepted;
+      if (diverged) {
+        set_status(v.status + p, DOCP_DIVERGENCE, DOCP_AT_SQP_ITERATE, cfg.iter + 1);
+      } else if (cfg.is_loop) {
+        v.step_sizes[static_cast<long>(p) * v.max_hist + cfg.iter] = alpha;
+        v.pcg_hist[static_cast<long>(p) * v.max_hist + cfg.iter] = v.pcg_iters[p];
+        v.sqp_iters[p] = cfg.iter + 1;
+        if (s_step <= cfg.conv_tol) v.converged[p] = 1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+/// ||kkt_residual(Z, LAMBDA)||_inf (problem.hpp:263-300), one CTA per problem.
+__global__ void kkt_kernel(View v, const int* __restrict__ work, const int* __restrict__ n_work) {
+  __shared__ unsigned long long s_max;
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, T = d.T;
+  const Family fam = Family::from(v.prob);
+  for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
+    const int p = work[w];
+    if (v.status[p].code != DOCP_OK) continue;
+    if (threadIdx.x == 0) s_max = 0ull;
+    __syncthreads();
+    const double* th = v.theta + static_cast<long>(p) * d.nth;
+    const double* z = v.z + static_cast<long>(p) * d.nz;
+    const double* lam = v.lam + static_cast<long>(p) * d.nl;
+    double m = 0.0;
+    for (int t = threadIdx.x; t <= T; t += blockDim.x) {
+      double jx[kMaxNx * kMaxNx], ju[kMaxNx * kMaxNx], res[kMaxNx];
+      const double* wx = fam.w_x(d, th);
+      // grad_l for x_t: cost grad, + lambda_t (A+_{t-1}' lambda_t, or lambda_0 last), + A_t' lambda_{t+1}
+      if (t < T) fam.dynamics(d, th, z + xoff(d, t + 1), z + xoff(d, t), z + uoff(d, t), res, jx, ju);
+      for (int i = 0; i < nx; ++i) {
+        double g = diag_cost_grad(fam.scale, wx[i], z[xoff(d, t) + i]);
+        double a = 0.0;
+        if (t < T) {
+          a = jx[i * nx] * lam[(t + 1) * nx];
+          for (int k = 1; k < nx; ++k) a = a + jx[k + i * nx] * lam[(t + 1) * nx + k];
+        }
+        if (t == 0) {
+          if (t < T) g = g + a;
+          g = g + lam[i];
+        } else {
+          g = g + lam[t * nx + i];
+          if (t < T) g = g + a;
+        }
+        m = fmax(m, fabs(g));
+      }
+      if (t < T) {
+        const double* wu = fam.w_u(d, th);
+        for (int i = 0; i < nu; ++i) {
+          double g = diag_cost_grad(fam.scale, wu[i], z[uoff(d, t) + i]);
+          double a = ju[i * nx] * lam[(t + 1) * nx];
+          for (int k = 1; k < nx; ++k) a = a + ju[k + i * nx] * lam[(t + 1) * nx + k];
+          m = fmax(m, fabs(g + a));
+        }
+        for (int i = 0; i < nx; ++i) m = fmax(m, fabs(res[i]));
+      } else {
+        const double* x_s = fam.x_s(d, th);
+        for (int i = 0; i < nx; ++i) m = fmax(m, fabs(z[i] - x_s[i]));
+      }
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_max, __double_as_longlong(m));
+    __syncthreads();
+    if (threadIdx.x == 0) v.kkt[p] = __longlong_as_double(s_max);
+    __syncthreads();
+  }
+}
+
+/// K4 epilogue: GRAD_THETA = theta_vjp(z, lambda, z~ = Z_QP, lambda~), one
+/// thread per theta entry folding over t in the reference's order.
+__global__ void vjp_kernel(View v, const int* __restrict__ work, const int* __restrict__ n_work) {
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, T = d.T;
+  const Family fam = Family::from(v.prob);
+  const double s2 = 2.0 * fam.scale;
+  const long total = static_cast<long>(*n_work) * d.nth;
+  for (long g = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int p = work[g / d.nth];
+    const int k = static_cast<int>(g % d.nth);
+    if (v.status[p].code != DOCP_OK) continue;
+    const double* z = v.z + static_cast<long>(p) * d.nz;
+    const double* zt = v.zqp + static_cast<long>(p) * d.nz;
+    const double* lam = v.lam + static_cast<long>(p) * d.nl;
+    const double* lt = v.lt + static_cast<long>(p) * d.nl;
+    double acc = 0.0;
+    if (k < nx) {  // state-cost weights
+      for (int t = 0; t <= T; ++t) acc = acc - s2 * (z[xoff(d, t) + k] * zt[xoff(d, t) + k]);
+    } else if (k < nx + nu) {
+      const int i = k - nx;
+      for (int t = 0; t < T; ++t) acc = acc - s2 * (z[uoff(d, t) + i] * zt[uoff(d, t) + i]);
+    } else if (fam.kind == DOCP_CARTPOLE) {  // initial state
+      acc = acc + lt[k - 5];
+    } else {
+      const int e = k - nx - nu;
+      if (e < nx * nx) {  // dA(i,j) += lam_{t+1,i} z~x_{t,j} + lam~_{t+1,i} x_{t,j}
+        const int i = e % nx, j = e / nx;
+        for (int t = 0; t < T; ++t) {
+          acc = acc + lam[(t + 1) * nx + i] * zt[xoff(d, t) + j];
+          acc = acc + lt[(t + 1) * nx + i] * z[xoff(d, t) + j];
+        }
+      } else if (e < nx * nx + nx * nu) {
+        const int f = e - nx * nx;
+        const int i = f % nx, j = f / nx;
+        for (int t = 0; t < T; ++t) {
+          acc = acc + lam[(t + 1) * nx + i] * zt[uoff(d, t) + j];
+          acc = acc + lt[(t + 1) * nx + i] * z[uoff(d, t) + j];
+        }
+      } else if (e < nx * nx + nx * nu + nx) {
+        const int i = e - nx * nx - nx * nu;
+        for (int t = 0; t < T; ++t) acc = acc + lt[(t + 1) * nx + i];
+      } else {
+        acc = acc + lt[e - nx * nx - nx * nu - nx];
+      }
+    }
+    v.grad[static_cast<long>(p) * d.nth + k] = acc;
+  }
+}
+
+/// IL epoch, before the solve: shared learnable segment -> every theta,
+/// z0 = demonstration (train.hpp:85-88).
+__global__ void il_setup_kernel(View v, const double* __restrict__ weights, int learn_start, int learn_size,
+                                const double* __restrict__ demos) {
+  const Dims d = v.d;
+  const long n = static_cast<long>(v.B) * (learn_size + d.nz);
+  for (long g = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; g < n;
+       g += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int p = static_cast<int>(g / (learn_size + d.nz));
+    const int k = static_cast<int>(g % (learn_size + d.nz));
+    if (k < learn_size) v.theta[static_cast<long>(p) * d.nth + learn_start + k] = weights[k];
+    else v.z[static_cast<long>(p) * d.nz + (k - learn_size)] = demos[static_cast<long>(p) * d.nz + (k - learn_size)];
+  }
+}
+
+/// IL epoch, after the solve: loss_j = |u - u^|^2 / den and its gradient in
+/// the flat layout (train.hpp:89-95), one thread per problem.
+__global__ void il_loss_kernel(View v, const double* __restrict__ demos, double den) {
+  const Dims d = v.d;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < v.B; p += gridDim.x * blockDim.x) {
+    const double* z = v.z + static_cast<long>(p) * d.nz;
+    const double* dm = demos + static_cast<long>(p) * d.nz;
+    double* lg = v.lgz + static_cast<long>(p) * d.nz;
+    double acc = 0.0;
+    bool first = true;
+    for (int e = 0; e < d.nz; ++e) lg[e] = 0.0;
+    for (int t = 0; t < d.T; ++t)
+      for (int i = 0; i < d.nu; ++i) {
+        const double du = z[uoff(d, t) + i] - dm[uoff(d, t) + i];
+        acc = first ? du * du : acc + du * du;
+        first = false;
+        lg[uoff(d, t) + i] = 2.0 / den * du;
+      }
+    v.loss[p] = acc / den;
+  }
+}
+
+/// Fixed-order (instance order) sums of the epoch (train.hpp:126-131):
+/// thread 0 sums the losses, thread 1+k the k-th learnable gradient entry.
+__global__ void il_sum_kernel(View v, int learn_start, int learn_size, double* __restrict__ loss_sum,
+                              double* __restrict__ grad_sum) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 0) {
+    double acc = 0.0;
+    for (int p = 0; p < v.B; ++p) acc = acc + v.loss[p];
+    *loss_sum = acc;
+  } else if (k - 1 < learn_size) {
+    double acc = 0.0;
+    for (int p = 0; p < v.B; ++p) acc = acc + v.grad[static_cast<long>(p) * v.d.nth + learn_start + k - 1];
+    grad_sum[k - 1] = acc;
+  }
+}
+
+}  // namespace docp_dev

@@ -1,0 +1,345 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle.
+
+The checker is the plain-C restatement (oracle/port), itself pinned
+bit-for-bit to the reference headers (tests/test_oracle_port.py). Bars:
+  * PARITY PCG mode: bit-identical z, lambda, lambda~, dtheta and equal
+    iteration counts (cart-pole: <= 1e-12 relative, device sin/cos differ from
+    glibc's by <= 2 ulp);
+  * FAST mode (FMA + tree reductions): equal PCG / SQP iteration counts and
+    <= 1e-9 relative error (north_star's fp64 bar).
+"""
+import numpy as np
+import pytest
+
+import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+RTOL_FAST = 1e-9
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(1.0, np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def D():
+    import paper_2510_06179_b200 as D
+    return D
+
+
+def aq_thetas(nx, nu, T, seed, count):
+    """random_convex_instance draws (generators.hpp:102-111) via the reference
+    when available, else the golden fixture set."""
+    if po.available("ref"):
+        return po.gen_aq(nx, nu, T, seed, count)
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        A = np.eye(nx) + 0.1 * rng.standard_normal((nx, nx))
+        rho = max(abs(np.linalg.eigvals(A)))
+        if rho > 0.99:
+            A *= 0.99 / rho
+        out.append(np.concatenate([rng.uniform(0.5, 2, nx), rng.uniform(0.5, 2, nu), A.T.ravel(),
+                                   rng.standard_normal((nu, nx)).ravel(), 1e-2 * rng.standard_normal(nx),
+                                   rng.standard_normal(nx)]))
+    return np.array(out)
+
+
+def port_problem(p):
+    if p.family == 2:
+        return po.cartpole_problem(p.horizon, p.cart_mass, p.pole_mass, p.length, p.gravity, p.dt)
+    return po.aq_problem(p.n_x, p.n_u, p.horizon, p.cost_scale)
+
+
+# ----------------------------------------------------------------- PCG KATs (test_pcg.cpp)
+
+
+def test_pcg_scalar_kat(D):
+    """test_pcg.cpp:46-61: gamma_stored = (-1, 0), lambda = (-1.5, -0.5), <= 2 iterations."""
+    prob = D.affine_quadratic(1, 1, 1, cost_scale=0.5)
+    theta = np.array([1.0, 1.0, 1.0, 1.0, 0.0, 1.0])
+    b = D.Batch(prob, 1)
+    b.upload(D._lib.F_THETA, theta)
+    b.upload(D._lib.F_Z, np.zeros(3))
+    b.linearize()
+    b.assemble_schur()
+    b.assemble_gamma()
+    g = b.download(D._lib.F_GAMMA)[0]
+    assert g[0] == pytest.approx(-1.0) and abs(g[1]) <= 1e-15
+    for mode in ("fast", "parity"):
+        b.upload(D._lib.F_LAMBDA, np.zeros(2))
+        b.pcg_solve(D.PcgConfig(mode=mode))
+        lam = b.download(D._lib.F_LAMBDA)[0]
+        assert b.download(D._lib.F_PCG_ITERS)[0, 0] <= 2
+        assert b.download(D._lib.F_PCG_CONVERGED)[0, 0] == 1
+        assert lam == pytest.approx([-1.5, -0.5])
+    sd, ss, pd, ps = b.download_schur()
+    assert sd[0, :, 0, 0] == pytest.approx([1.0, 3.0]) and ss[0, 0, 0, 0] == pytest.approx(-1.0)
+    assert pd[0, :, 0, 0] == pytest.approx([1.0, 1.0 / 3.0]) and ps[0, 0, 0, 0] == pytest.approx(1.0 / 3.0)
+
+
+@pytest.mark.parametrize("nx,T", [(3, 5), (4, 6), (8, 4)])
+def test_pcg_identity_system_one_iteration(D, nx, T):
+    """test_pcg.cpp:32-44: a decoupled instance gives -S = Phi^-1 = I."""
+    prob = D.affine_quadratic(nx, nx, T, cost_scale=0.5)
+    theta = np.concatenate([np.ones(2 * nx), np.zeros(2 * nx * nx + 2 * nx)])
+    b = D.Batch(prob, 2)
+    b.upload(D._lib.F_THETA, np.tile(theta, (2, 1)))
+    b.upload(D._lib.F_Z, np.zeros((2, b.nz)))
+    b.linearize()
+    b.assemble_schur()
+    rng = np.random.default_rng(1)
+    gamma = rng.standard_normal((2, b.nl))
+    b.upload(D._lib.F_GAMMA, gamma)
+    for mode in ("fast", "parity"):
+        b.upload(D._lib.F_LAMBDA, np.zeros((2, b.nl)))
+        b.pcg_solve(D.PcgConfig(mode=mode))
+        assert (b.download(D._lib.F_PCG_ITERS)[:, 0] == 1).all()
+        assert np.abs(b.download(D._lib.F_LAMBDA) - gamma).max() < 1e-12
+
+
+def test_pcg_breakdown_and_cap(D):
+    """test_pcg.cpp:162-190: indefinite system -> BreakdownError(iteration 0);
+    max_iters = 2 -> 2 iterations, unconverged."""
+    prob = D.affine_quadratic(2, 2, 3, cost_scale=0.5)
+    b = D.Batch(prob, 1)
+    nb = 4
+    eye = np.tile(np.eye(2), (1, nb, 1, 1))
+    zero = np.zeros((1, nb - 1, 2, 2))
+    b.upload_schur(-eye, zero, eye, zero)
+    b.upload(D._lib.F_GAMMA, np.ones((1, b.nl)))
+    b.upload(D._lib.F_LAMBDA, np.zeros((1, b.nl)))
+    b.pcg_solve(D.PcgConfig())
+    err = b.errors()[0]
+    assert isinstance(err, D.BreakdownError) and err.iteration == 0
+
+    th = aq_thetas(8, 4, 30, 7, 1)
+    p2 = D.affine_quadratic(8, 4, 30)
+    b2 = D.Batch(p2, 1)
+    b2.upload(D._lib.F_THETA, th)
+    b2.upload(D._lib.F_Z, np.zeros((1, b2.nz)))
+    b2.linearize()
+    b2.assemble_schur()
+    b2.upload(D._lib.F_GAMMA, np.random.default_rng(7).standard_normal((1, b2.nl)))
+    b2.upload(D._lib.F_LAMBDA, np.zeros((1, b2.nl)))
+    b2.pcg_solve(D.PcgConfig(epsilon=1e-14, max_iters=2))
+    assert b2.download(D._lib.F_PCG_ITERS)[0, 0] == 2
+    assert b2.download(D._lib.F_PCG_CONVERGED)[0, 0] == 0
+
+
+@pytest.mark.parametrize("nx,nu,T,seed", [(4, 2, 10, 1), (8, 4, 30, 2), (8, 4, 100, 3), (6, 3, 12, 4),
+                                          (16, 8, 30, 5), (9, 2, 40, 6)])
+def test_pcg_on_oracle_blocks(D, nx, nu, T, seed):
+    """K2 alone: blocks and gamma assembled by the oracle; PARITY is
+    bit-identical to the oracle's pcg_solve, FAST within 1e-9 with equal
+    iteration counts."""
+    th = aq_thetas(nx, nu, T, seed, 3)
+    pp = po.aq_problem(nx, nu, T)
+    o = po.Oracle("port", pp)
+    blocks, gammas, want = [], [], []
+    for j in range(3):
+        o.linearize(th[j], np.zeros(o.nz))
+        o.assemble()
+        g = o.gamma(o.flat_b(), o.flat_d())
+        blocks.append(o.schur())
+        gammas.append(g)
+        want.append(o.pcg(g, np.zeros(o.nl)))
+    b = D.Batch(D.affine_quadratic(nx, nu, T), 3)
+    b.upload_schur(*[np.stack([bl[k] for bl in blocks]) for k in range(4)])
+    b.upload(D._lib.F_GAMMA, np.stack(gammas))
+    for mode in ("parity", "fast"):
+        b.upload(D._lib.F_LAMBDA, np.zeros((3, b.nl)))
+        b.pcg_solve(D.PcgConfig(mode=mode))
+        lam = b.download(D._lib.F_LAMBDA)
+        its = b.download(D._lib.F_PCG_ITERS)[:, 0]
+        for j in range(3):
+            assert its[j] == want[j][1], (mode, j, its[j], want[j][1])
+            if mode == "parity":
+                assert np.array_equal(lam[j], want[j][0])
+            else:
+                assert rel(lam[j], want[j][0]) <= RTOL_FAST
+
+
+# ----------------------------------------------------------------- K1 assembly
+
+
+@pytest.mark.parametrize("nx,nu,T,seed", [(1, 1, 1, 0), (4, 2, 20, 1), (8, 4, 100, 2), (5, 2, 9, 3),
+                                          (16, 8, 30, 4)])
+def test_assembly_bitwise(D, nx, nu, T, seed):
+    """linearize + assemble_schur + assemble_gamma at a random z are
+    bit-identical to the oracle (diagonal Hessians specialised exactly)."""
+    th = aq_thetas(nx, nu, T, seed, 2)
+    rng = np.random.default_rng(seed)
+    prob = D.affine_quadratic(nx, nu, T)
+    b = D.Batch(prob, 2)
+    z = rng.standard_normal((2, b.nz))
+    b.upload(D._lib.F_THETA, th)
+    b.upload(D._lib.F_Z, z)
+    b.linearize()
+    b.assemble_schur()
+    b.assemble_gamma()
+    blocks = b.download_schur()
+    qp = b.download_qp()
+    gam = b.download(D._lib.F_GAMMA)
+    for j in range(2):
+        o = po.Oracle("port", po.aq_problem(nx, nu, T))
+        o.linearize(th[j], z[j])
+        o.assemble()
+        want = o.schur()
+        for k in range(4):
+            assert np.array_equal(blocks[k][j], want[k]), k
+        oq = o.qp()
+        for k in ("Q", "q", "R", "r", "A", "B", "C", "x_s"):
+            assert np.array_equal(qp[k][j], oq[k]), k
+        assert np.array_equal(gam[j], o.gamma(o.flat_b(), o.flat_d()))
+
+
+def test_assembly_cartpole(D):
+    x0, demos = _cartpole_demos(4)
+    prob = D.cartpole(40)
+    b = D.Batch(prob, 4)
+    th = np.array([np.concatenate([[1, 2, 1.5, 1], [0.05], x]) for x in x0])
+    z = demos * 0.97
+    b.upload(D._lib.F_THETA, th)
+    b.upload(D._lib.F_Z, z)
+    b.linearize()
+    b.assemble_schur()
+    blocks = b.download_schur()
+    for j in range(4):
+        o = po.Oracle("port", po.cartpole_problem(40))
+        o.linearize(th[j], z[j])
+        o.assemble()
+        want = o.schur()
+        for k in range(4):
+            assert rel(blocks[k][j], want[k]) <= 1e-12
+
+
+# ----------------------------------------------------------------- full SQP + backward
+
+
+def _cartpole_demos(n, T=40, seed=0):
+    if po.available("ref"):
+        return po.gen_cartpole(seed, T, n)
+    import json, os
+    path = os.path.join(os.path.dirname(__file__), "golden", f"cartpole_T{T}_seed{seed}.npz")
+    g = np.load(path)
+    return g["x0"][:n], g["demos"][:n]
+
+
+def _oracle_solve_and_grad(pprob, th, z0, lam0, cfg_port, lg, lt0):
+    o = po.Oracle("port", pprob)
+    s = o.sqp_solve(th, z0, lam0, cfg_port)
+    g, lt, it = o.backward(th, lg, lt0)
+    return s, g, lt, it
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+@pytest.mark.parametrize("nx,nu,T,seed,max_it", [(4, 2, 20, 11, 20), (8, 4, 30, 12, 20), (8, 4, 100, 13, 5),
+                                                 (3, 2, 4, 14, 20), (16, 8, 30, 15, 20)])
+def test_sqp_backward_affine_quadratic(D, mode, nx, nu, T, seed, max_it):
+    B = 4
+    th = aq_thetas(nx, nu, T, seed, B)
+    prob = D.affine_quadratic(nx, nu, T)
+    rng = np.random.default_rng(seed)
+    nz, nl = D.sizes(prob)
+    z0 = rng.standard_normal((B, nz))
+    lg = rng.standard_normal((B, nz))
+    cfg = D.SqpConfig(max_sqp_iters=max_it, pcg=D.PcgConfig(mode=mode))
+    res, errs = D.sqp_solve_batch(prob, th, z0, np.zeros((B, nl)), cfg)
+    assert all(e is None for e in errs)
+    b = res[0].batch
+    grads, lts, its, errs = D.backward_vjp_batch(b, lg, np.zeros((B, nl)), cfg.pcg)
+    assert all(e is None for e in errs)
+    for j in range(B):
+        s, g, lt, it = _oracle_solve_and_grad(po.aq_problem(nx, nu, T), th[j], z0[j], np.zeros(nl),
+                                              po.sqp_config(max_sqp_iters=max_it), lg[j], np.zeros(nl))
+        assert res[j].sqp_iters == s.sqp_iters and res[j].pcg_iters == s.pcg_iters and its[j] == it
+        assert res[j].converged == s.converged
+        if mode == "parity":
+            assert np.array_equal(res[j].z, s.z) and np.array_equal(res[j].lam, s.lam)
+            assert np.array_equal(grads[j], g) and np.array_equal(lts[j], lt)
+            assert res[j].kkt_inf_norm == s.kkt and res[j].step_sizes == s.step_sizes
+        else:
+            for got, want in ((res[j].z, s.z), (res[j].lam, s.lam), (grads[j], g), (lts[j], lt)):
+                assert rel(got, want) <= RTOL_FAST
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_sqp_backward_cartpole(D, mode):
+    B, T = 6, 40
+    x0, demos = _cartpole_demos(B, T)
+    prob = D.cartpole(T)
+    nz, nl = D.sizes(prob)
+    w = np.array([0.3, 0.8, 0.5, 0.9])
+    th = np.array([np.concatenate([w, [0.05], x]) for x in x0])
+    cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(mode=mode))
+    res, errs = D.sqp_solve_batch(prob, th, demos, np.zeros((B, nl)), cfg)
+    assert all(e is None for e in errs)
+    lg = np.zeros((B, nz))
+    for j in range(B):
+        for t in range(T):
+            k = D.flat_offset(4, 1, t, False)
+            lg[j, k] = 2.0 / B * (res[j].z[k] - demos[j, k])
+    grads, lts, its, errs = D.backward_vjp_batch(res[0].batch, lg, np.zeros((B, nl)), cfg.pcg)
+    for j in range(B):
+        s, g, lt, it = _oracle_solve_and_grad(po.cartpole_problem(T), th[j], demos[j], np.zeros(nl),
+                                              po.sqp_config(max_sqp_iters=5), lg[j], np.zeros(nl))
+        assert res[j].sqp_iters == s.sqp_iters and res[j].pcg_iters == s.pcg_iters and its[j] == it
+        tol = 1e-12 if mode == "parity" else RTOL_FAST
+        for got, want in ((res[j].z, s.z), (res[j].lam, s.lam), (grads[j], g), (lts[j], lt)):
+            assert rel(got, want) <= tol
+
+
+def test_il_epoch_matches_oracle(D):
+    """One train_il epoch body (C3 shape, scaled down): per-instance solve from
+    the demonstration, MSE loss, warm-started backward, fixed-order sums."""
+    import torch
+    nx, nu, T, B = 8, 4, 30, 16
+    th = aq_thetas(nx, nu, T, 21, B)
+    prob = D.affine_quadratic(nx, nu, T)
+    nz, nl = D.sizes(prob)
+    expert = np.array([1, 2, 1.5, 1, 1, 2, 1.5, 1.0])
+    th[:, :nx] = expert
+    pp = po.aq_problem(nx, nu, T)
+    demos = np.array([po.Oracle("port", pp).sqp_solve(th[j], np.zeros(nz), np.zeros(nl), po.sqp_config()).z
+                      for j in range(B)])
+    w = np.random.default_rng(0).uniform(0, 1, nx)
+    cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(mode="parity"))
+    b = D.Batch(prob, B)
+    b.upload(D._lib.F_THETA, th)
+    dev = torch.device("cuda")
+    wt = torch.tensor(w, device=dev)
+    demos_t = torch.tensor(demos, device=dev)
+    loss_t = torch.zeros(1, dtype=torch.float64, device=dev)
+    grad_t = torch.zeros(nx, dtype=torch.float64, device=dev)
+    lam_c, lt_c = np.zeros((B, nl)), np.zeros((B, nl))
+    for epoch in range(2):
+        b.il_epoch(cfg, wt.data_ptr(), 0, nx, demos_t.data_ptr(), float(B), loss_t.data_ptr(), grad_t.data_ptr())
+        b.sync()
+        th_e = th.copy()
+        th_e[:, :nx] = w
+        loss, grad, *_ = po.il_epoch("port", pp, th_e, demos, lam_c, lt_c, po.sqp_config(max_sqp_iters=5), 0, nx)
+        assert loss_t.item() == loss
+        assert np.array_equal(grad_t.cpu().numpy(), grad)
+        assert np.array_equal(b.download(D._lib.F_LAMBDA), lam_c)
+        assert np.array_equal(b.download(D._lib.F_LAMBDA_TILDE), lt_c)
+        w = w - 1e-2 * grad
+        wt = torch.tensor(w, device=dev)
+
+
+def test_error_statuses(D):
+    """Per-problem failures become the reference's errors; the rest of the
+    batch is unaffected (batch.hpp:92-101)."""
+    nx, nu, T = 4, 2, 10
+    th = aq_thetas(nx, nu, T, 31, 3)
+    th[1, -nx] = np.nan  # non-finite x_s (test_batch.cpp:88-105)
+    prob = D.affine_quadratic(nx, nu, T)
+    nz, nl = D.sizes(prob)
+    res, errs = D.sqp_solve_batch(prob, th, np.zeros((3, nz)), np.zeros((3, nl)), D.SqpConfig())
+    assert errs[0] is None and errs[2] is None
+    assert isinstance(errs[1], D.EvaluationError) and "initial_state" in str(errs[1])
+    with pytest.raises(D.DimensionError):
+        D.sqp_solve(prob, th[0], np.full(nz, np.inf), np.zeros(nl))
+    with pytest.raises(D.DimensionError):
+        D.sqp_solve(prob, th[0], np.zeros(nz), np.zeros(nl), D.SqpConfig(step_candidates=(1.0, 1.0)))
