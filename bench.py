@@ -1,0 +1,394 @@
+#!/usr/bin/env python3
+"""bench.py — BASELINE.json's metric on its C3 configuration.
+
+"OCP solve+gradient problems/sec (batch 4096, T=100) at 1/2/4/8 B200; PCG HBM %"
+
+A step is one imitation-learning epoch (the train_il epoch body,
+train.hpp:82-145) over 4096 random_convex_instance(8, 4, 100) problems per
+GPU: per instance a warm-started SQP solve (max 5 iterations, PCG eps 1e-12)
+from its expert demonstration, the control-matching loss, one adjoint PCG
+solve + theta-VJP, then the fixed-order gradient sum, its exchange across
+GPUs (NCCL all-gather, rank-order sum) and the gradient step on the shared
+state-cost weights. value = problems/s over all GPUs (weak scaling: 4096 per
+GPU), timed on the device with CUDA events, max over ranks.
+
+    python bench.py [--gpus N --steps K --warmup W]        our CUDA path
+    python bench.py --impl reference ...                   the reference CPU solver
+                                                           (oracle/_ref) on the host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "OCP solve+gradient problems/sec (batch 4096, T=100) at 1/2/4/8 B200; PCG HBM %"
+NX, NU, T = 8, 4, 100
+EXPERT_W = np.array([1.0, 2.0, 1.5, 1.0, 1.0, 2.0, 1.5, 1.0])  # shared expert weights
+LR = 1e-2                                                     # IlTrainOptions (train.hpp:38-46)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=4096, help="problems per GPU")
+    ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU time of the baseline sample")
+    return ap.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            pk = json.load(fh)
+        return pk.get("hbm_gbs", 6650.0), "measured", pk.get("sm_max_mhz", 1965.0)
+    return 6650.0, "fallback", 1965.0
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
+                "power_w_max": max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()),
+                "samples": len(self.rows), "reasons": reasons}
+
+
+# --------------------------------------------------------------------------- reference arm (CPU)
+
+
+def reference_sample(n, seed=0):
+    """The reference's own inputs: its generators and its own expert solves."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    prob = po.aq_problem(NX, NU, T)
+    nz, nl = po.sizes(prob)
+    th = po.gen_aq(NX, NU, T, seed, n)
+    th[:, :NX] = EXPERT_W
+    demos = np.array([po.Oracle("ref", prob).sqp_solve(th[j], np.zeros(nz), np.zeros(nl), po.sqp_config()).z
+                      for j in range(n)])
+    return po, prob, th, demos
+
+
+def cpu_epochs(po, prob, th, demos, w0, epochs, kind):
+    """train_il epochs (train.hpp:76-145) on the host cores via the checker."""
+    n = th.shape[0]
+    nz, nl = po.sizes(prob)
+    lam, lt = np.zeros((n, nl)), np.zeros((n, nl))
+    w = w0.copy()
+    times = []
+    for _ in range(epochs):
+        th_e = th.copy()
+        th_e[:, :NX] = w
+        t0 = time.perf_counter()
+        loss, grad, *_ = po.il_epoch(kind, prob, th_e, demos, lam, lt, po.sqp_config(max_sqp_iters=5), 0, NX)
+        times.append(time.perf_counter() - t0)
+        w = w - LR * grad
+    return times
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def measure_cpu_baseline(target_s, kind="reference"):
+    """Bounded sample of the C3 workload on the host cores (warm epoch timed)."""
+    cores = cpu_cores()
+    os.environ["DOCP_WORKERS"] = str(cores)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    if kind == "reference" and not po.available("ref"):
+        kind = "port"
+    n = cores
+    po_, prob, th, demos = reference_sample(n) if kind == "reference" else _port_sample(po, n)
+    t = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 1, kind)[0]
+    n = int(min(4096, max(cores, cores * round(target_s / 2 / max(t, 1e-3)))))
+    po_, prob, th, demos = reference_sample(n) if kind == "reference" else _port_sample(po, n)
+    times = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 2, kind)
+    return {"value": n / times[1], "unit": "problems/s", "cores": cores, "kind": kind,
+            "sample": f"{n} of the 4096 C3 problems (random_convex_instance(8,4,100), seed 0), one warm IL epoch "
+                      f"(second of two) through parallel_for with {cores} workers: {times[1]:.2f} s"}
+
+
+def _port_sample(po, n):
+    prob = po.aq_problem(NX, NU, T)
+    import paper_2510_06179_b200 as D  # generator only (host code)
+    nz, nl = po.sizes(prob)
+    th = D.generate_affine_quadratic(NX, NU, 0, n)
+    th[:, :NX] = EXPERT_W
+    demos = np.array([po.Oracle("port", prob).sqp_solve(th[j], np.zeros(nz), np.zeros(nl), po.sqp_config()).z
+                      for j in range(n)])
+    return po, prob, th, demos
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = cpu_cores()
+    os.environ["DOCP_WORKERS"] = str(cores)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    if not po.available("ref"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference here)"}))
+        return 0
+    # size one epoch to ~ a few seconds on this host
+    po_, prob, th, demos = reference_sample(cores)
+    t1 = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 1, "ref")[0]
+    per_epoch_target = 150.0 / max(1, args.steps + args.warmup)
+    n = int(min(args.batch, max(cores, cores * round(per_epoch_target / 2 / max(t1, 1e-3)))))
+    po_, prob, th, demos = reference_sample(n)
+    import paper_2510_06179_b200 as D  # host-side uniform draw only (train.hpp:61-64 recipe)
+    w0 = D.generate_uniform(0, NX)
+    times = cpu_epochs(po_, prob, th, demos, w0, args.warmup + args.steps, "ref")[args.warmup:]
+    secs = float(np.sum(times))
+    value = n * args.steps / secs
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: the reference's random_convex_instance(8,4,100) draws (mt19937_64 seed 0) with "
+                    "its own expert demonstrations",
+            "config": {"workload": "C3 imitation-learning epoch (train_il body) on a bounded sample",
+                       "batch_per_step": n, "horizon": T, "n_x": NX, "n_u": NU, "max_sqp_iters": 5,
+                       "pcg_epsilon": 1e-12},
+            "cpu_baseline": {"value": value, "unit": "problems/s", "cores": cores, "kind": "reference",
+                             "sample": f"{n} problems per epoch, reference headers + eigen_lite, parallel_for "
+                                       f"with {cores} workers"},
+            "e2e": {"value": value, "unit": "problems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------- our CUDA path
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_06179_b200 as D
+    from paper_2510_06179_b200 import _lib as L
+    from paper_2510_06179_b200.distributed import fixed_order_allreduce
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    B = args.batch
+    prob = D.affine_quadratic(NX, NU, T)
+    nz, nl = D.sizes(prob)
+    nth = D.theta_size(prob)
+    # this rank's contiguous shard of one sequential draw (generators.hpp:102-111)
+    th_all = D.generate_affine_quadratic(NX, NU, 0, B * world)
+    thetas = th_all[rank * B:(rank + 1) * B].copy()
+
+    # expert demonstrations: sqp_solve at theta* (default SqpConfig), on the GPU, untimed
+    expert = thetas.copy()
+    expert[:, :NX] = EXPERT_W
+    b = D.Batch(prob, B, local)
+    b.set_stream(stream.cuda_stream)
+    b.upload(L.F_THETA, expert)
+    b.upload(L.F_Z, np.zeros((B, nz)))
+    b.upload(L.F_LAMBDA, np.zeros((B, nl)))
+    b.sqp_solve(D.SqpConfig(pcg=D.PcgConfig(mode=args.mode)))
+    errs = [e for e in b.errors() if e is not None]
+    if errs:
+        raise RuntimeError(f"expert solves failed: {errs[0]}")
+    demos_host = b.download(L.F_Z)
+    demos = torch.tensor(demos_host, device=dev)
+
+    # training state: learned shared weights ~ U[0,1]^8 (train.hpp:61-64), caches zero
+    w = torch.tensor(D.generate_uniform(0, NX), device=dev)
+    b.upload(L.F_THETA, thetas)
+    b.upload(L.F_LAMBDA, np.zeros((B, nl)))
+    b.upload(L.F_LAMBDA_TILDE, np.zeros((B, nl)))
+    out = torch.zeros(1 + NX, dtype=torch.float64, device=dev)  # [loss | grad]
+    cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode=args.mode))
+    den = float(B * world)
+
+    def epoch():
+        b.il_epoch(cfg, w.data_ptr(), 0, NX, demos.data_ptr(), den, out.data_ptr(), out.data_ptr() + 8)
+        tot = fixed_order_allreduce(out) if world > 1 else out
+        w.sub_(LR * tot[1:])
+        return tot
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        epoch()
+    barrier()
+    launches0 = D.kernel_launches()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            tot = epoch()
+        stop.record(stream)
+        barrier()
+    launches = D.kernel_launches() - launches0
+    ms = start.elapsed_time(stop)
+    loss_last = float(tot[0].item())
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = B * world * args.steps / (ms_max / 1e3)
+
+    # per-kernel profile of the same steps (CUDA events on the launching stream)
+    b.profile_begin()
+    for _ in range(args.steps):
+        epoch()
+    prof = b.profile_end()
+    pcg_ms = prof["kernels"]["pcg"]["ms"]
+    total_kernel_ms = sum(k["ms"] for k in prof["kernels"].values())
+    peak, peak_kind, sm_max = load_peaks()
+    achieved = prof["pcg_algorithmic_bytes"] / (pcg_ms / 1e3) / 1e9 if pcg_ms > 0 else 0.0
+    smem_peak = 148 * 128 * sm_max * 1e6 / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "pcg_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    solves = max(1, prof["pcg_solves"])
+
+    # e2e: the same epochs through the C ABI with host buffers (pinned), copies timed
+    th_pin = torch.tensor(thetas).pin_memory()
+    demos_pin = torch.tensor(demos_host).pin_memory()
+    w_pin = w.cpu().pin_memory()
+    res_pin = torch.zeros(1 + NX, dtype=torch.float64).pin_memory()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        b.upload(L.F_THETA, th_pin.numpy())          # docp_batch_upload (host -> device)
+        demos.copy_(demos_pin, non_blocking=True)
+        w.copy_(w_pin, non_blocking=True)
+        tot = epoch()
+        res_pin.copy_(tot, non_blocking=True)
+        stream.synchronize()
+        w_pin = (w_pin - LR * res_pin[1:]).contiguous()
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    et = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = B * world * args.steps / (float(et.item()) / 1e3)
+    h2d = thetas.nbytes + demos_host.nbytes + 8 * NX
+    d2h = 8 * (1 + NX)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = measure_cpu_baseline(args.cpu_seconds)
+        except Exception as exc:  # reported, never fatal
+            cpu = {"value": None, "unit": "problems/s", "cores": cpu_cores(), "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: random_convex_instance(8,4,100) draws (reference recipe, mt19937_64 seed 0), "
+                    "expert demonstrations solved on the GPU at w*",
+            "config": {"workload": "C3 imitation-learning epoch (train_il body): solve + adjoint gradient + "
+                                   "fixed-order sum + theta-gradient exchange + GD step",
+                       "batch_per_gpu": B, "global_batch": B * world, "horizon": T, "n_x": NX, "n_u": NU,
+                       "max_sqp_iters": 5, "pcg_epsilon": 1e-12, "pcg_mode": args.mode,
+                       "parallelism": f"dp{world} (instance sharding)",
+                       "l2": "inputs larger than L2: %.0f MB of Schur blocks per GPU" %
+                             (B * 2 * (2 * T + 1) * NX * NX * 8 / 1e6)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "kernel": "pcg_kernel<8,1,fast,resident>",
+                         "algorithmic_bytes_per_iteration": prof["pcg_bytes_per_iteration"],
+                         "note": "blocks are SMEM-resident (TMA-staged once per solve), so algorithmic GB/s "
+                                 "exceeds HBM; binding roofline is SMEM",
+                         "smem_peak_derived": smem_peak, "frac_smem": achieved / smem_peak},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "problems/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "clocks": clocks.summary(),
+            "gpu_launches": launches,
+            "profile": {"kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof["kernels"].items()},
+                        "launches_per_step": {k: v["launches"] / args.steps for k, v in prof["kernels"].items()},
+                        "pcg_share_of_kernel_time": pcg_ms / total_kernel_ms if total_kernel_ms else None,
+                        "pcg_iterations_per_solve": prof["pcg_iterations"] / solves,
+                        "pcg_solves_per_step": prof["pcg_solves"] / args.steps,
+                        "loss_last_step": loss_last},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -29,7 +29,7 @@ def build_cuda(force=False, verbose=False):
     if not force and not _stale(LIB, sources):
         return
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB, os.path.join(CSRC, "docp_cuda.cu")]
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB, os.path.join(CSRC, "docp_cuda.cu"), os.path.join(CSRC, "generators.cpp")]
     log = os.path.join(os.path.dirname(LIB), "ptxas.log")
     with open(log, "w") as fh:
         r = subprocess.run(cmd, stdout=fh, stderr=subprocess.STDOUT)

@@ -211,6 +211,31 @@ int docp_il_epoch(docp_batch* batch, const docp_sqp_config* cfg, const double* w
                   int32_t learn_size, const double* demos, double loss_denominator, double* loss_sum,
                   double* grad_sum);
 
+/* ---- synthetic inputs (the reference generators' recipe, generators.hpp) -- */
+/* count sequential random_convex_instance (convex != 0) / random_linear_instance
+ * draws from mt19937_64(seed), as thetas ([count][n_theta], host memory). */
+int docp_generate_affine_quadratic(int32_t n_x, int32_t n_u, uint64_t seed, int32_t count, int32_t convex,
+                                   double* thetas);
+int docp_generate_uniform(uint64_t seed, int32_t n, double lo, double hi, double* out);
+/* gen_cartpole initial states (generators.hpp:142-152), [n][4]. */
+int docp_generate_cartpole_x0(uint64_t seed, int32_t n, double* x0);
+
+/* ---- profiling: CUDA events around every launch on the batch stream ------ */
+enum docp_prof_kind {
+  DOCP_PROF_ASSEMBLE = 0, DOCP_PROF_GAMMA = 1, DOCP_PROF_PCG = 2, DOCP_PROF_RECOVER = 3,
+  DOCP_PROF_STEP = 4, DOCP_PROF_KKT = 5, DOCP_PROF_VJP = 6, DOCP_PROF_KINDS = 7
+};
+typedef struct docp_profile {
+  int32_t launches[DOCP_PROF_KINDS];
+  double ms[DOCP_PROF_KINDS];            /* summed launch durations */
+  uint64_t pcg_iterations;               /* PCG iterations performed */
+  uint64_t pcg_solves;                   /* PCG solves performed */
+  double pcg_bytes_per_iteration;        /* B_it = 16 n_x^2 (2T+1) */
+  double pcg_algorithmic_bytes;          /* (iterations + solves) B_it + solves 24 n_lambda */
+} docp_profile;
+int docp_profile_begin(docp_batch* batch);
+int docp_profile_end(docp_batch* batch, docp_profile* out);
+
 /* ---- diagnostics --------------------------------------------------------- */
 uint64_t docp_pcg_invocations(void);      /* PCG system solves performed (one per problem per solve) */
 uint64_t docp_kernel_launches(void);      /* kernels this library has launched */

@@ -44,6 +44,16 @@ class SqpConfigC(C.Structure):
                 ("mu_floor_denominator", C.c_double), ("eps_pd", C.c_double)]
 
 
+PROF_KINDS = 7
+PROF_NAMES = ("assemble", "gamma", "pcg", "recover", "step", "kkt", "vjp")
+
+
+class Profile(C.Structure):
+    _fields_ = [("launches", C.c_int32 * PROF_KINDS), ("ms", C.c_double * PROF_KINDS),
+                ("pcg_iterations", C.c_uint64), ("pcg_solves", C.c_uint64),
+                ("pcg_bytes_per_iteration", C.c_double), ("pcg_algorithmic_bytes", C.c_double)]
+
+
 # every symbol include/docp_cuda.h declares, with its ctypes signature
 _vp, _i32, _u64, _dbl, _sz = C.c_void_p, C.c_int32, C.c_uint64, C.c_double, C.c_size_t
 _dp = C.POINTER(C.c_double)
@@ -71,6 +81,11 @@ SIGNATURES = {
     "docp_sqp_solve": (C.c_int, [_vp, C.POINTER(SqpConfigC)]),
     "docp_backward_vjp": (C.c_int, [_vp, C.POINTER(PcgConfigC)]),
     "docp_il_epoch": (C.c_int, [_vp, C.POINTER(SqpConfigC), _vp, _i32, _i32, _vp, _dbl, _vp, _vp]),
+    "docp_generate_affine_quadratic": (C.c_int, [_i32, _i32, _u64, _i32, _i32, _dp]),
+    "docp_generate_uniform": (C.c_int, [_u64, _i32, _dbl, _dbl, _dp]),
+    "docp_generate_cartpole_x0": (C.c_int, [_u64, _i32, _dp]),
+    "docp_profile_begin": (C.c_int, [_vp]),
+    "docp_profile_end": (C.c_int, [_vp, C.POINTER(Profile)]),
     "docp_pcg_invocations": (_u64, []),
     "docp_kernel_launches": (_u64, []),
     "docp_last_error": (C.c_char_p, []),

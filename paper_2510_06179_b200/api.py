@@ -180,6 +180,31 @@ def kernel_launches() -> int:
     return int(L.lib().docp_kernel_launches())
 
 
+# --------------------------------------------------------------------------- synthetic inputs
+
+
+def generate_affine_quadratic(n_x: int, n_u: int, seed: int, count: int, convex: bool = True) -> np.ndarray:
+    """Sequential random_convex_instance / random_linear_instance draws
+    (generators.hpp:52-111) as thetas [count][n_theta]."""
+    out = np.zeros((count, n_x + n_u + n_x * n_x + n_x * n_u + 2 * n_x))
+    _raise_call(L.lib().docp_generate_affine_quadratic(n_x, n_u, seed, count, 1 if convex else 0,
+                                                       out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+def generate_uniform(seed: int, n: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+    out = np.zeros(n)
+    _raise_call(L.lib().docp_generate_uniform(seed, n, lo, hi, out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+def generate_cartpole_x0(seed: int, n: int) -> np.ndarray:
+    """gen_cartpole initial states (generators.hpp:142-152)."""
+    out = np.zeros((n, 4))
+    _raise_call(L.lib().docp_generate_cartpole_x0(seed, n, out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
 # --------------------------------------------------------------------------- batch
 
 _FLOAT_FIELDS = {L.F_THETA, L.F_Z, L.F_LAMBDA, L.F_LAMBDA_TILDE, L.F_LOSS_GRAD_Z, L.F_GRAD_THETA, L.F_GAMMA,
@@ -269,6 +294,18 @@ class Batch:
         for k in ("Q", "R", "A", "B"):
             out[k] = np.ascontiguousarray(np.swapaxes(out[k], -1, -2))
         return out
+
+    # ---- profiling (CUDA events around every launch on the batch stream)
+    def profile_begin(self):
+        _raise_call(L.lib().docp_profile_begin(self.h))
+
+    def profile_end(self) -> dict:
+        p = L.Profile()
+        _raise_call(L.lib().docp_profile_end(self.h, C.byref(p)))
+        kinds = {n: {"launches": int(p.launches[i]), "ms": float(p.ms[i])} for i, n in enumerate(L.PROF_NAMES)}
+        return {"kernels": kinds, "pcg_iterations": int(p.pcg_iterations), "pcg_solves": int(p.pcg_solves),
+                "pcg_bytes_per_iteration": float(p.pcg_bytes_per_iteration),
+                "pcg_algorithmic_bytes": float(p.pcg_algorithmic_bytes)}
 
     # ---- primitives (one call each for the whole batch)
     def linearize(self, eps_pd: float = 1e-6):

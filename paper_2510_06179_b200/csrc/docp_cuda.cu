@@ -68,8 +68,14 @@ struct docp_batch {
   std::vector<void*> allocs;
   int max_hist = 0;
   double last_eps_pd = 1e-6;
+  // profiling: CUDA events around every launch, per kernel kind, on the batch stream
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[DOCP_PROF_KINDS];
+  std::vector<cudaEvent_t> event_pool;
+  size_t pool_used = 0;
 
   ~docp_batch() {
+    for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (h_count) cudaFreeHost(h_count);
   }
@@ -101,6 +107,32 @@ int grid_for(long items, int threads, int cap_blocks = 1 << 20) {
   long g = (items + threads - 1) / threads;
   return static_cast<int>(std::max<long>(1, std::min<long>(g, cap_blocks)));
 }
+
+cudaEvent_t pool_event(docp_batch* b) {
+  if (b->pool_used == b->event_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    b->event_pool.push_back(e);
+  }
+  return b->event_pool[b->pool_used++];
+}
+
+/// RAII scope recording a (start, stop) event pair around one launch.
+struct ProfScope {
+  docp_batch* b;
+  int kind;
+  cudaEvent_t stop = nullptr;
+  ProfScope(docp_batch* bb, int k) : b(bb), kind(k) {
+    if (!b->profiling) return;
+    cudaEvent_t start = pool_event(b);
+    stop = pool_event(b);
+    cudaEventRecord(start, b->stream);
+    b->prof[kind].emplace_back(start, stop);
+  }
+  ~ProfScope() {
+    if (stop) cudaEventRecord(stop, b->stream);
+  }
+};
 
 // ---------------------------------------------------------------- kernels of the driver
 __global__ void init_solve_kernel(View v, int* __restrict__ list, int* __restrict__ count) {
@@ -160,12 +192,14 @@ int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint
     attr_set = true;
   }
   const int grid = std::max(1, std::min(n_hint, b->num_sms * 8));
+  ProfScope ps(b, DOCP_PROF_ASSEMBLE);
   assemble_kernel<<<grid, kAsmThreads, smem, b->stream>>>(b->v, list, count, eps_pd, do_schur);
   LAUNCH_CHECK();
   return DOCP_OK;
 }
 
 int launch_gamma(docp_batch* b, const int* list, const int* count, int n_hint, int rhs) {
+  ProfScope ps(b, DOCP_PROF_GAMMA);
   gamma_kernel<<<grid_for(static_cast<long>(n_hint) * b->d.nl, 256, b->num_sms * 16), 256, 0, b->stream>>>(
       b->v, list, count, rhs);
   LAUNCH_CHECK();
@@ -173,6 +207,7 @@ int launch_gamma(docp_batch* b, const int* list, const int* count, int n_hint, i
 }
 
 int launch_recover(docp_batch* b, const int* list, const int* count, int n_hint, const double* lam, int rhs) {
+  ProfScope ps(b, DOCP_PROF_RECOVER);
   recover_kernel<<<grid_for(static_cast<long>(n_hint) * b->d.nz, 256, b->num_sms * 16), 256, 0, b->stream>>>(
       b->v, list, count, lam, rhs);
   LAUNCH_CHECK();
@@ -219,6 +254,7 @@ int launch_pcg_t(docp_batch* b, const PcgPlan& pl, const int* list, const int* c
   if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit on an SM (smem %zu)", pl.smem);
   const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
   CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
+  ProfScope ps(b, DOCP_PROF_PCG);
   kern<<<grid, pl.threads, pl.smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
   LAUNCH_CHECK();
   return DOCP_OK;
@@ -277,12 +313,14 @@ int launch_step(docp_batch* b, const docp_sqp_config& cfg, const int* list, cons
   CUDA_TRY(cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   if (smem > 200 * 1024) return fail(DOCP_UNSUPPORTED, "line search: horizon too long");
   const int grid = std::max(1, std::min(n_hint, b->num_sms * 8));
+  ProfScope ps(b, DOCP_PROF_STEP);
   step_kernel<<<grid, kStepThreads, smem, b->stream>>>(b->v, list, count, sc);
   LAUNCH_CHECK();
   return DOCP_OK;
 }
 
 int launch_kkt(docp_batch* b, const int* list, const int* count, int n_hint) {
+  ProfScope ps(b, DOCP_PROF_KKT);
   kkt_kernel<<<std::max(1, std::min(n_hint, b->num_sms * 8)), 64, 0, b->stream>>>(b->v, list, count);
   LAUNCH_CHECK();
   return DOCP_OK;
@@ -428,6 +466,7 @@ int docp_batch_create(const docp_problem* problem, int32_t batch_size, int32_t d
   A(b->list[0], B);
   A(b->list[1], B);
   A(b->counts, 8);
+  A(v.pcg_acc, 2);
 #undef A
   if ((rc = ensure_hist(b, 20))) {
     delete b;
@@ -675,6 +714,7 @@ int docp_backward_vjp(docp_batch* b, const docp_pcg_config* cfg) {  // backward.
   if ((rc = launch_gamma(b, list, cnt, b->B, DOCP_RHS_ADJOINT))) return rc;
   if ((rc = launch_pcg(b, *cfg, list, cnt, b->B, b->v.lt))) return rc;
   if ((rc = launch_recover(b, list, cnt, b->B, b->v.lt, DOCP_RHS_ADJOINT))) return rc;
+  ProfScope ps(b, DOCP_PROF_VJP);
   vjp_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 128, b->num_sms * 16), 128, 0, b->stream>>>(b->v, list,
                                                                                                         cnt);
   LAUNCH_CHECK();
@@ -697,6 +737,43 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
   il_sum_kernel<<<grid_for(learn_size + 1, 64, 64), 64, 0, b->stream>>>(b->v, learn_start, learn_size, loss_sum,
                                                                          grad_sum);
   LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+int docp_profile_begin(docp_batch* b) {
+  if (!b) return fail(DOCP_INVALID, "null batch");
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  for (auto& v : b->prof) v.clear();
+  b->pool_used = 0;
+  CUDA_TRY(cudaMemsetAsync(b->v.pcg_acc, 0, 2 * sizeof(unsigned long long), b->stream));
+  b->profiling = true;
+  return DOCP_OK;
+}
+
+int docp_profile_end(docp_batch* b, docp_profile* out) {
+  if (!b || !out) return fail(DOCP_INVALID, "null argument");
+  b->profiling = false;
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  std::memset(out, 0, sizeof *out);
+  for (int k = 0; k < DOCP_PROF_KINDS; ++k) {
+    out->launches[k] = static_cast<int32_t>(b->prof[k].size());
+    double ms = 0.0;
+    for (auto& ev : b->prof[k]) {
+      float t = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t, ev.first, ev.second));
+      ms += t;
+    }
+    out->ms[k] = ms;
+  }
+  unsigned long long acc[2];
+  CUDA_TRY(cudaMemcpy(acc, b->v.pcg_acc, sizeof acc, cudaMemcpyDeviceToHost));
+  out->pcg_iterations = acc[0];
+  out->pcg_solves = acc[1];
+  const Dims& d = b->d;
+  const double b_it = 16.0 * d.bsz * (2.0 * d.T + 1.0);  // symmetric -S + Phi^-1, fp64
+  out->pcg_bytes_per_iteration = b_it;
+  out->pcg_algorithmic_bytes =
+      (static_cast<double>(acc[0]) + static_cast<double>(acc[1])) * b_it + static_cast<double>(acc[1]) * 24.0 * d.nl;
   return DOCP_OK;
 }
 

@@ -390,6 +390,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads) pcg_kernel(View v, const int* 
       v.pcg_conv[p] = status == DOCP_OK && eta <= threshold;
       if (status == DOCP_OK) set_status(v.status + p, DOCP_OK, DOCP_AT_NONE, 0);
       else set_status(v.status + p, DOCP_BREAKDOWN, status, iters);
+      atomicAdd(v.pcg_acc, static_cast<unsigned long long>(iters));
+      atomicAdd(v.pcg_acc + 1, 1ull);
     }
     __syncthreads();
   }
