@@ -40,7 +40,7 @@ LR = 1e-2                                                     # IlTrainOptions (
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=4096, help="problems per GPU")
@@ -62,7 +62,7 @@ def load_peaks():
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -83,15 +83,26 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+            if len(parts) == 8:
+                self.rows.append((time.time(), parts[1:]))
 
     def __exit__(self, *exc):
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
+    def mark(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
     def summary(self):
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", time.time())
+        rows = [r for (ts, r) in self.rows if t0 <= ts <= t1 + 0.15]
+        if not rows:  # timed region shorter than one sample period: nearest samples
+            rows = [r for (ts, r) in sorted(self.rows, key=lambda x: abs(x[0] - t0))[:2]]
+        self.rows = rows
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -150,12 +161,13 @@ def measure_cpu_baseline(target_s, kind="reference"):
     import pyoracle as po
     if kind == "reference" and not po.available("ref"):
         kind = "port"
+    lib_kind = "ref" if kind == "reference" else "port"
     n = cores
     po_, prob, th, demos = reference_sample(n) if kind == "reference" else _port_sample(po, n)
-    t = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 1, kind)[0]
+    t = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 1, lib_kind)[0]
     n = int(min(4096, max(cores, cores * round(target_s / 2 / max(t, 1e-3)))))
     po_, prob, th, demos = reference_sample(n) if kind == "reference" else _port_sample(po, n)
-    times = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 2, kind)
+    times = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 2, lib_kind)
     return {"value": n / times[1], "unit": "problems/s", "cores": cores, "kind": kind,
             "sample": f"{n} of the 4096 C3 problems (random_convex_instance(8,4,100), seed 0), one warm IL epoch "
                       f"(second of two) through parallel_for with {cores} workers: {times[1]:.2f} s"}
@@ -279,12 +291,15 @@ def run_ours(args):
     launches0 = D.kernel_launches()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        time.sleep(0.3)  # sampler warm-up
         barrier()
+        clocks.mark(True)
         start.record(stream)
         for _ in range(args.steps):
             tot = epoch()
         stop.record(stream)
         barrier()
+        clocks.mark(False)
     launches = D.kernel_launches() - launches0
     ms = start.elapsed_time(stop)
     loss_last = float(tot[0].item())

@@ -24,18 +24,39 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
+UNITS = ["docp_cuda.cu", "pcg_nx8.cu", "pcg_nx4.cu", "pcg_nxrt.cu", "generators.cpp"]
+
+
 def build_cuda(force=False, verbose=False):
+    """Compiles the translation units in parallel, then links the shared library."""
     sources = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "docp_cuda.h")]
     if not force and not _stale(LIB, sources):
         return
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB, os.path.join(CSRC, "docp_cuda.cu"), os.path.join(CSRC, "generators.cpp")]
-    log = os.path.join(os.path.dirname(LIB), "ptxas.log")
-    with open(log, "w") as fh:
-        r = subprocess.run(cmd, stdout=fh, stderr=subprocess.STDOUT)
+    objdir = os.path.join(os.path.dirname(LIB), "obj")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    procs = []
+    for unit in UNITS:
+        obj = os.path.join(objdir, unit + ".o")
+        log = open(os.path.join(objdir, unit + ".log"), "w")
+        cmd = ["nvcc", *compile_flags, "-c", "-o", obj, os.path.join(CSRC, unit)]
+        procs.append((unit, obj, log, subprocess.Popen(cmd, stdout=log, stderr=subprocess.STDOUT)))
+    failed = []
+    for unit, obj, log, p in procs:
+        if p.wait() != 0:
+            failed.append(unit)
+        log.close()
+    with open(os.path.join(os.path.dirname(LIB), "ptxas.log"), "w") as out:
+        for unit in UNITS:
+            out.write(open(os.path.join(objdir, unit + ".log")).read())
+    if failed:
+        for unit in failed:
+            sys.stderr.write(open(os.path.join(objdir, unit + ".log")).read())
+        raise RuntimeError(f"nvcc failed: {failed}")
+    objs = [os.path.join(objdir, u + ".o") for u in UNITS]
+    r = subprocess.run(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs])
     if r.returncode != 0:
-        sys.stderr.write(open(log).read())
-        raise RuntimeError("nvcc failed")
+        raise RuntimeError("link failed")
     if verbose:
         print("built", LIB)
 

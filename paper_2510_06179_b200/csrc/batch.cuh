@@ -1,0 +1,115 @@
+// batch.cuh — the device-resident batch object and the host launch helpers
+// shared by the translation units of libdocp_cuda.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace docp_host {
+
+extern std::atomic<uint64_t> g_pcg_invocations;
+extern std::atomic<uint64_t> g_launches;
+int fail(int code, const char* fmt, ...);
+
+}  // namespace docp_host
+
+#define CUDA_TRY(expr)                                                                                   \
+  do {                                                                                                   \
+    cudaError_t e_ = (expr);                                                                             \
+    if (e_ != cudaSuccess) return docp_host::fail(DOCP_CUDA_ERROR, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                                                   \
+  do {                                                                                                   \
+    docp_host::g_launches.fetch_add(1, std::memory_order_relaxed);                                       \
+    cudaError_t e_ = cudaGetLastError();                                                                 \
+    if (e_ != cudaSuccess) return docp_host::fail(DOCP_CUDA_ERROR, "kernel launch: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+struct docp_batch {
+  docp_problem prob{};
+  docp_dev::Dims d{};
+  int B = 0;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  docp_dev::View v{};
+  // work lists: all problems, and two ping-pong active lists
+  int* all_list = nullptr;
+  int* list[2] = {nullptr, nullptr};
+  int* counts = nullptr;  // [0] all, [1] list0, [2] list1, [3] pcg queue counter
+  int* h_count = nullptr; // pinned
+  std::vector<void*> allocs;
+  int max_hist = 0;
+  double last_eps_pd = 1e-6;
+  // profiling: CUDA events around every launch, per kernel kind, on the batch stream
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[DOCP_PROF_KINDS];
+  std::vector<cudaEvent_t> event_pool;
+  size_t pool_used = 0;
+
+  ~docp_batch() {
+    for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
+    for (void* p : allocs) cudaFree(p);
+    if (h_count) cudaFreeHost(h_count);
+  }
+};
+
+namespace docp_host {
+
+inline int grid_for(long items, int threads, int cap_blocks = 1 << 20) {
+  long g = (items + threads - 1) / threads;
+  return static_cast<int>(std::max<long>(1, std::min<long>(g, cap_blocks)));
+}
+
+inline cudaEvent_t pool_event(docp_batch* b) {
+  if (b->pool_used == b->event_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    b->event_pool.push_back(e);
+  }
+  return b->event_pool[b->pool_used++];
+}
+
+/// RAII scope recording a (start, stop) event pair around one launch.
+struct ProfScope {
+  docp_batch* b;
+  int kind;
+  cudaEvent_t stop = nullptr;
+  ProfScope(docp_batch* bb, int k) : b(bb), kind(k) {
+    if (!b->profiling) return;
+    cudaEvent_t start = pool_event(b);
+    stop = pool_event(b);
+    cudaEventRecord(start, b->stream);
+    b->prof[kind].emplace_back(start, stop);
+  }
+  ~ProfScope() {
+    if (stop) cudaEventRecord(stop, b->stream);
+  }
+};
+
+struct PcgPlan {
+  bool resident;
+  int threads;
+  int maxr;
+  size_t smem;
+};
+
+// per-block-size PCG launchers (pcg_nx*.cu, compiled in parallel)
+#define DOCP_PCG_LAUNCHER(name)                                                                                \
+  int name(docp_batch* b, const PcgPlan& pl, bool par, const int* list, const int* count, int n_hint, double* sol, \
+           double eps, int max_iters)
+DOCP_PCG_LAUNCHER(launch_pcg_nx4);
+DOCP_PCG_LAUNCHER(launch_pcg_nx8);
+DOCP_PCG_LAUNCHER(launch_pcg_nxrt);
+
+}  // namespace docp_host

@@ -16,6 +16,7 @@ namespace docp_dev {
 constexpr int kMaxNx = 16;
 constexpr int kMaxNu = 16;
 constexpr int kWarp = 32;
+constexpr int kPcgMaxThreads = 256;  // K2: one thread per block row (MAXB block rows per thread beyond)
 
 /// Problem dimensions and per-problem strides (in doubles) of every field.
 struct Dims {
@@ -33,29 +34,31 @@ __host__ __device__ inline int xoff(const Dims& d, int t) { return t * (d.nx + d
 __host__ __device__ inline int uoff(const Dims& d, int t) { return t * (d.nx + d.nu) + d.nx; }
 
 /// Device block layout (DESIGN.md §HBM layout). A block is stored column
-/// by column (segment s' = physical column, NX doubles); columns and 16-byte
-/// chunks are permuted per block so that the PCG kernel's column reads
-/// (LDS.128, 8 lanes of one block row) and row reads (LDS.64, one column per
-/// step across the 4 or 8 block rows of a warp) are bank-conflict free:
-///   NX = 8: s' = s ^ (b & 1),      chunk' = chunk ^ ((s' >> 1) & 3)
-///   NX = 4: s' = (s + b) & 3,      chunk' = chunk ^ (b & 1)
+/// by column (physical column s', NX doubles each), with the 16-byte chunks of
+/// a column and the columns themselves permuted per block index b so that the
+/// PCG kernel (one thread per block row: 8 consecutive threads read 8
+/// consecutive blocks at the same logical (column, chunk)) is shared-memory
+/// bank-conflict free — every quarter-warp LDS.128 touches 8 distinct 4-bank
+/// groups:
+///   NX = 8: s' = s ^ ((b >> 2) & 1),   chunk' = chunk ^ (b & 3)
+///   NX = 4: s' = s ^ (b & 3),          chunk' = chunk ^ ((b >> 2) & 1)
 ///   other : plain column-major.
 __host__ __device__ inline int blk_off(int nx, int b, int e, int s) {
   if (nx == 8) {
-    const int sp = s ^ (b & 1);
-    return sp * 8 + ((((e >> 1) ^ ((sp >> 1) & 3)) << 1) | (e & 1));
+    const int sp = s ^ ((b >> 2) & 1);
+    return sp * 8 + ((((e >> 1) ^ (b & 3)) << 1) | (e & 1));
   }
   if (nx == 4) {
-    const int sp = (s + b) & 3;
-    return sp * 4 + ((((e >> 1) ^ (b & 1)) << 1) | (e & 1));
+    const int sp = s ^ (b & 3);
+    return sp * 4 + ((((e >> 1) ^ ((b >> 2) & 1)) << 1) | (e & 1));
   }
   return s * nx + e;
 }
 
-/// Iterate-vector layout in shared memory (block j, entry e): the same idea
-/// for the 8-lane broadcast reads of v_{i-1}, v_i, v_{i+1}.
+/// Iterate-vector layout in shared memory (block j, entry e): conflict-free
+/// LDS.128/STS.128 by 8 consecutive block rows.
 __host__ __device__ inline int vec_off(int nx, int j, int e) {
-  if (nx == 8) return j * 8 + ((((e >> 1) ^ (((j >> 1) & 1) << 1)) << 1) | (e & 1));
+  if (nx == 8) return j * 8 + ((((e >> 1) ^ ((j >> 1) & 3)) << 1) | (e & 1));
   if (nx == 4) return j * 4 + ((((e >> 1) ^ ((j >> 2) & 1)) << 1) | (e & 1));
   return j * nx + e;
 }

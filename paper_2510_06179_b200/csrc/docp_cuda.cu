@@ -13,15 +13,15 @@
 #include <string>
 #include <vector>
 
-#include "common.cuh"
+#include "batch.cuh"
 #include "families.cuh"
 #include "k_assemble.cuh"
-#include "k_pcg.cuh"
 #include "k_step.cuh"
 
 using namespace docp_dev;
+using namespace docp_host;
 
-namespace {
+namespace docp_host {
 
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_pcg_invocations{0};
@@ -37,49 +37,7 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
-#define CUDA_TRY(expr)                                                                       \
-  do {                                                                                       \
-    cudaError_t e_ = (expr);                                                                 \
-    if (e_ != cudaSuccess) return fail(DOCP_CUDA_ERROR, "%s: %s", #expr, cudaGetErrorString(e_)); \
-  } while (0)
-
-#define LAUNCH_CHECK()                                                                       \
-  do {                                                                                       \
-    g_launches.fetch_add(1, std::memory_order_relaxed);                                      \
-    cudaError_t e_ = cudaGetLastError();                                                     \
-    if (e_ != cudaSuccess) return fail(DOCP_CUDA_ERROR, "kernel launch: %s", cudaGetErrorString(e_)); \
-  } while (0)
-
-}  // namespace
-
-struct docp_batch {
-  docp_problem prob{};
-  Dims d{};
-  int B = 0;
-  int device = 0;
-  int num_sms = 148;
-  cudaStream_t stream = nullptr;
-  View v{};
-  // work lists: all problems, and two ping-pong active lists
-  int* all_list = nullptr;
-  int* list[2] = {nullptr, nullptr};
-  int* counts = nullptr;  // [0] all, [1] list0, [2] list1, [3] pcg queue counter
-  int* h_count = nullptr; // pinned
-  std::vector<void*> allocs;
-  int max_hist = 0;
-  double last_eps_pd = 1e-6;
-  // profiling: CUDA events around every launch, per kernel kind, on the batch stream
-  bool profiling = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[DOCP_PROF_KINDS];
-  std::vector<cudaEvent_t> event_pool;
-  size_t pool_used = 0;
-
-  ~docp_batch() {
-    for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
-    for (void* p : allocs) cudaFree(p);
-    if (h_count) cudaFreeHost(h_count);
-  }
-};
+}  // namespace docp_host
 
 namespace {
 
@@ -102,37 +60,6 @@ int ensure_hist(docp_batch* b, int n) {
   b->v.max_hist = n;
   return DOCP_OK;
 }
-
-int grid_for(long items, int threads, int cap_blocks = 1 << 20) {
-  long g = (items + threads - 1) / threads;
-  return static_cast<int>(std::max<long>(1, std::min<long>(g, cap_blocks)));
-}
-
-cudaEvent_t pool_event(docp_batch* b) {
-  if (b->pool_used == b->event_pool.size()) {
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    b->event_pool.push_back(e);
-  }
-  return b->event_pool[b->pool_used++];
-}
-
-/// RAII scope recording a (start, stop) event pair around one launch.
-struct ProfScope {
-  docp_batch* b;
-  int kind;
-  cudaEvent_t stop = nullptr;
-  ProfScope(docp_batch* bb, int k) : b(bb), kind(k) {
-    if (!b->profiling) return;
-    cudaEvent_t start = pool_event(b);
-    stop = pool_event(b);
-    cudaEventRecord(start, b->stream);
-    b->prof[kind].emplace_back(start, stop);
-  }
-  ~ProfScope() {
-    if (stop) cudaEventRecord(stop, b->stream);
-  }
-};
 
 // ---------------------------------------------------------------- kernels of the driver
 __global__ void init_solve_kernel(View v, int* __restrict__ list, int* __restrict__ count) {
@@ -183,14 +110,30 @@ __global__ void reset_status_kernel(View v) {
 }
 
 // ---------------------------------------------------------------- launch helpers
+template <int NX, int NU>
+int launch_assemble_t(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur) {
+  constexpr int NG = kAsmGroupThreads / NX;
+  const size_t smem = static_cast<size_t>(NG) * (4 * NX * NX + 2 * NX * NU) * sizeof(double);
+  auto kern = assemble_kernel_t<NX, NU>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAsmGroupThreads, smem));
+  const int grid = std::max(1, std::min(n_hint, std::max(1, per_sm) * b->num_sms));
+  ProfScope ps(b, DOCP_PROF_ASSEMBLE);
+  kern<<<grid, kAsmGroupThreads, smem, b->stream>>>(b->v, list, count, eps_pd, do_schur);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
 int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur) {
+  const int nx = b->d.nx, nu = b->d.nu;
+  if (nx == 8 && nu == 4) return launch_assemble_t<8, 4>(b, list, count, n_hint, eps_pd, do_schur);
+  if (nx == 8 && nu == 2) return launch_assemble_t<8, 2>(b, list, count, n_hint, eps_pd, do_schur);
+  if (nx == 4 && nu == 2) return launch_assemble_t<4, 2>(b, list, count, n_hint, eps_pd, do_schur);
+  if (nx == 4 && nu == 1) return launch_assemble_t<4, 1>(b, list, count, n_hint, eps_pd, do_schur);
   const int sp = std::max(b->d.bsz, b->d.nx * b->d.nu);
   const size_t smem = static_cast<size_t>(kAsmWarps) * 6 * sp * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set = true;
-  }
+  CUDA_TRY(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   const int grid = std::max(1, std::min(n_hint, b->num_sms * 8));
   ProfScope ps(b, DOCP_PROF_ASSEMBLE);
   assemble_kernel<<<grid, kAsmThreads, smem, b->stream>>>(b->v, list, count, eps_pd, do_schur);
@@ -214,85 +157,37 @@ int launch_recover(docp_batch* b, const int* list, const int* count, int n_hint,
   return DOCP_OK;
 }
 
-// ---- PCG variant selection
-struct PcgPlan {
-  bool resident;
-  int threads;
-  int maxr;
-  size_t smem;
-};
-
-size_t pcg_smem(const Dims& d, bool resident, bool parity) {
+size_t pcg_smem(const Dims& d, bool resident) {
   auto up2 = [](long n) { return (n + 1) & ~1L; };
-  long dbl = 2 * up2(d.nl) + 64;
-  if (parity) dbl += up2(d.nl) + up2(d.nb);
+  long dbl = 3 * up2(d.nl) + 64;  // vbuf, xbuf, seg/prod + reduction
   if (resident) dbl += d.blk_stride;
   return static_cast<size_t>(dbl) * sizeof(double);
 }
 
-PcgPlan plan_pcg(const docp_batch* b, bool parity) {
+PcgPlan plan_pcg(const docp_batch* b) {
   PcgPlan pl{};
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device);
   const size_t static_smem = 64;
-  pl.resident = pcg_smem(b->d, true, parity) + static_smem <= static_cast<size_t>(max_optin);
-  pl.smem = pcg_smem(b->d, pl.resident, parity);
-  const int nl = b->d.nl;
-  pl.threads = std::min(kPcgMaxThreads, (nl + 31) / 32 * 32);
-  const int need = (nl + pl.threads - 1) / pl.threads;
-  pl.maxr = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : 0;
+  pl.resident = pcg_smem(b->d, true) + static_smem <= static_cast<size_t>(max_optin);
+  pl.smem = pcg_smem(b->d, pl.resident);
+  const int nb = b->d.nb;  // one thread per block row (MAXB block rows beyond 256)
+  pl.threads = std::min(kPcgMaxThreads, (nb + 31) / 32 * 32);
+  const int need = (nb + pl.threads - 1) / pl.threads;
+  pl.maxr = need <= 1 ? 1 : need <= 2 ? 2 : 0;
   return pl;
-}
-
-template <int NX, int MAXR, bool PAR, bool RES>
-int launch_pcg_t(docp_batch* b, const PcgPlan& pl, const int* list, const int* count, int n_hint, double* sol,
-                 double eps, int max_iters) {
-  auto kern = pcg_kernel<NX, MAXR, PAR, RES>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)));
-  int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl.threads, pl.smem));
-  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit on an SM (smem %zu)", pl.smem);
-  const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
-  CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
-  ProfScope ps(b, DOCP_PROF_PCG);
-  kern<<<grid, pl.threads, pl.smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
-  LAUNCH_CHECK();
-  return DOCP_OK;
-}
-
-template <int NX, bool PAR, bool RES>
-int launch_pcg_r(docp_batch* b, const PcgPlan& pl, const int* list, const int* count, int n_hint, double* sol,
-                 double eps, int max_iters) {
-  switch (pl.maxr) {
-    case 1: return launch_pcg_t<NX, 1, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
-    case 2: return launch_pcg_t<NX, 2, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
-    case 4: return launch_pcg_t<NX, 4, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
-    case 8: return launch_pcg_t<NX, 8, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
-    default: return fail(DOCP_UNSUPPORTED, "pcg: system dimension %d too large", b->d.nl);
-  }
-}
-
-template <int NX>
-int launch_pcg_nx(docp_batch* b, const PcgPlan& pl, bool par, const int* list, const int* count, int n_hint,
-                  double* sol, double eps, int max_iters) {
-  if (par) {
-    return pl.resident ? launch_pcg_r<NX, true, true>(b, pl, list, count, n_hint, sol, eps, max_iters)
-                       : launch_pcg_r<NX, true, false>(b, pl, list, count, n_hint, sol, eps, max_iters);
-  }
-  return pl.resident ? launch_pcg_r<NX, false, true>(b, pl, list, count, n_hint, sol, eps, max_iters)
-                     : launch_pcg_r<NX, false, false>(b, pl, list, count, n_hint, sol, eps, max_iters);
 }
 
 int launch_pcg(docp_batch* b, const docp_pcg_config& cfg, const int* list, const int* count, int n_hint,
                double* sol) {
   if (!(cfg.epsilon > 0.0 && cfg.max_iters >= 0)) return fail(DOCP_DIMENSION, "pcg: invalid config");
   const bool par = cfg.mode == DOCP_PCG_PARITY;
-  const PcgPlan pl = plan_pcg(b, par);
+  const PcgPlan pl = plan_pcg(b);
   g_pcg_invocations.fetch_add(static_cast<uint64_t>(n_hint), std::memory_order_relaxed);
   switch (b->d.nx) {
-    case 4: return launch_pcg_nx<4>(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
-    case 8: return launch_pcg_nx<8>(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
-    default: return launch_pcg_nx<0>(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+    case 4: return launch_pcg_nx4(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+    case 8: return launch_pcg_nx8(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+    default: return launch_pcg_nxrt(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
   }
 }
 
@@ -810,7 +705,7 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   int dev = 0, max_optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const bool res = pcg_smem(d, true, false) + 64 <= static_cast<size_t>(max_optin);
+  const bool res = pcg_smem(d, true) + 64 <= static_cast<size_t>(max_optin);
   return snprintf(buf, cap, "nx=%d layout=%s pcg=%s record=%ld B", d.nx,
                   d.nx == 8 ? "swizzle8" : d.nx == 4 ? "swizzle4" : "colmajor", res ? "resident(TMA)" : "streaming",
                   d.blk_stride * 8);

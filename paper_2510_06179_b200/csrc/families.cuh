@@ -3,10 +3,12 @@
 //
 // Every expression keeps the reference's evaluation order so that, compiled
 // with --fmad=false, stage values are bit-identical to the reference headers
-// (cart-pole's sin/cos aside: CUDA's are within 2 ulp of glibc's).
+// (cart-pole's sin/cos aside: crmath.cuh's are correctly rounded; glibc's
+// misround ~0.1% of arguments by one ulp).
 #pragma once
 
 #include "common.cuh"
+#include "crmath.cuh"
 
 namespace docp_dev {
 
@@ -69,8 +71,8 @@ struct Family {
       return;
     }
     // cart-pole: make_explicit_dynamics(cartpole_step), cartpole.hpp:28-78
-    const double sn = sin(x[2]);
-    const double c = cos(x[2]);
+    double sn, c;  // correctly rounded (crmath.cuh): glibc-equivalent except at its rare misroundings
+    crmath::sincos_cr(x[2], &sn, &c);
     const double mp = pole_mass;
     const double len = length;
     const double g = gravity;
