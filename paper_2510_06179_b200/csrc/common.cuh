@@ -34,18 +34,18 @@ __host__ __device__ inline int xoff(const Dims& d, int t) { return t * (d.nx + d
 __host__ __device__ inline int uoff(const Dims& d, int t) { return t * (d.nx + d.nu) + d.nx; }
 
 /// Device block layout (DESIGN.md §HBM layout). A block is stored column
-/// by column (physical column s', NX doubles each), with the 16-byte chunks of
-/// a column and the columns themselves permuted per block index b so that the
-/// PCG kernel (one thread per block row: 8 consecutive threads read 8
-/// consecutive blocks at the same logical (column, chunk)) is shared-memory
-/// bank-conflict free — every quarter-warp LDS.128 touches 8 distinct 4-bank
-/// groups:
-///   NX = 8: s' = s ^ ((b >> 2) & 1),   chunk' = chunk ^ (b & 3)
-///   NX = 4: s' = s ^ (b & 3),          chunk' = chunk ^ ((b >> 2) & 1)
+/// by column (physical column s', NX doubles each); the 16-byte chunks of a
+/// column and the columns are permuted per block index b so that the PCG
+/// kernels' shared-memory reads are bank-conflict free (each quarter-warp
+/// LDS.128 touches 8 distinct 4-bank groups):
+///   NX = 8: s' = s ^ (b & 1),   chunk' = chunk ^ (b & 3)
+///           (pcg_kernel_h8: two threads per block row; see its access orders)
+///   NX = 4: s' = s ^ (b & 3),   chunk' = chunk ^ ((b >> 2) & 1)
+///           (pcg_kernel: one thread per block row)
 ///   other : plain column-major.
 __host__ __device__ inline int blk_off(int nx, int b, int e, int s) {
   if (nx == 8) {
-    const int sp = s ^ ((b >> 2) & 1);
+    const int sp = s ^ (b & 1);
     return sp * 8 + ((((e >> 1) ^ (b & 3)) << 1) | (e & 1));
   }
   if (nx == 4) {

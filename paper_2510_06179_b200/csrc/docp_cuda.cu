@@ -159,7 +159,7 @@ int launch_recover(docp_batch* b, const int* list, const int* count, int n_hint,
 
 size_t pcg_smem(const Dims& d, bool resident) {
   auto up2 = [](long n) { return (n + 1) & ~1L; };
-  long dbl = 3 * up2(d.nl) + 64;  // vbuf, xbuf, seg/prod + reduction
+  long dbl = 3 * up2(d.nl) + up2(d.nb) + 64;  // vbuf, xbuf, products + block dots, reduction
   if (resident) dbl += d.blk_stride;
   return static_cast<size_t>(dbl) * sizeof(double);
 }
