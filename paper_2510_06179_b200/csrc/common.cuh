@@ -28,7 +28,15 @@ struct Dims {
   int bsz;  // n_x * n_x
   // block region offsets inside one problem's block record (doubles)
   long s_diag, s_sub, p_diag, p_sup, blk_stride;
+  // stage Jacobian storage A_t [nx*nx], B_t [nx*nu]: families whose Jacobians
+  // do not depend on t or z (affine-quadratic: A_t = -A, B_t = -B) keep one
+  // copy per problem (stride 0 over t)
+  long a_per, a_stride, b_per, b_stride;
 };
+
+/// A_t / B_t of problem p (column-major).
+__host__ __device__ inline long a_off(const Dims& d, int p, int t) { return p * d.a_per + t * d.a_stride; }
+__host__ __device__ inline long b_off(const Dims& d, int p, int t) { return p * d.b_per + t * d.b_stride; }
 
 __host__ __device__ inline int xoff(const Dims& d, int t) { return t * (d.nx + d.nu); }  // trajectory.hpp:72-74
 __host__ __device__ inline int uoff(const Dims& d, int t) { return t * (d.nx + d.nu) + d.nx; }
@@ -80,6 +88,11 @@ inline Dims make_dims(const docp_problem& p) {
   d.p_diag = d.s_sub + off;
   d.p_sup = d.p_diag + diag;
   d.blk_stride = (d.p_sup + off + 31) & ~31L;  // 256-byte aligned records
+  const bool tv = p.family != DOCP_AFFINE_QUADRATIC;
+  d.a_stride = tv ? d.bsz : 0;
+  d.b_stride = tv ? static_cast<long>(d.nx) * d.nu : 0;
+  d.a_per = tv ? static_cast<long>(d.T) * d.bsz : d.bsz;
+  d.b_per = tv ? static_cast<long>(d.T) * d.nx * d.nu : static_cast<long>(d.nx) * d.nu;
   return d;
 }
 

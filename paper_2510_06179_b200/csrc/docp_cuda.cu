@@ -113,7 +113,7 @@ __global__ void reset_status_kernel(View v) {
 template <int NX, int NU>
 int launch_assemble_t(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur) {
   constexpr int NG = kAsmGroupThreads / NX;
-  const size_t smem = static_cast<size_t>(NG) * (4 * NX * NX + 2 * NX * NU) * sizeof(double);
+  const size_t smem = static_cast<size_t>(NG) * (5 * NX * NX + 2 * NX * NU) * sizeof(double);
   auto kern = assemble_kernel_t<NX, NU>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
@@ -143,8 +143,9 @@ int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint
 
 int launch_gamma(docp_batch* b, const int* list, const int* count, int n_hint, int rhs) {
   ProfScope ps(b, DOCP_PROF_GAMMA);
-  gamma_kernel<<<grid_for(static_cast<long>(n_hint) * b->d.nl, 256, b->num_sms * 16), 256, 0, b->stream>>>(
-      b->v, list, count, rhs);
+  const size_t smem = (static_cast<size_t>(b->d.nb) * b->d.nx + static_cast<size_t>(b->d.T) * b->d.nu) * 8;
+  CUDA_TRY(cudaFuncSetAttribute(gamma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  gamma_kernel<<<std::max(1, std::min(n_hint, b->num_sms * 8)), 128, smem, b->stream>>>(b->v, list, count, rhs);
   LAUNCH_CHECK();
   return DOCP_OK;
 }
@@ -340,8 +341,8 @@ int docp_batch_create(const docp_problem* problem, int32_t batch_size, int32_t d
   A(v.rd, B * d.T * d.nu);
   A(v.lr, B * d.T * d.nu);
   A(v.r, B * d.T * d.nu);
-  A(v.A, B * d.T * d.bsz);
-  A(v.Bm, B * d.T * d.nx * d.nu);
+  A(v.A, B * d.a_per);
+  A(v.Bm, B * d.b_per);
   A(v.C, B * d.T * d.nx);
   A(v.xs, B * d.nx);
   A(v.blocks, B * d.blk_stride);
@@ -506,9 +507,16 @@ int docp_batch_download_qp(docp_batch* b, double* Q, double* q, double* R, doubl
     return DOCP_OK;
   };
   if ((rc = copy(q, b->v.q, B * d.nb * d.nx)) || (rc = copy(r, b->v.r, B * d.T * d.nu)) ||
-      (rc = copy(A, b->v.A, B * d.T * d.bsz)) || (rc = copy(Bm, b->v.Bm, B * d.T * d.nx * d.nu)) ||
       (rc = copy(C, b->v.C, B * d.T * d.nx)) || (rc = copy(x_s, b->v.xs, B * d.nx)))
     return rc;
+  std::vector<double> a, bm;
+  if ((rc = fetch(b->v.A, B * d.a_per, a)) || (rc = fetch(b->v.Bm, B * d.b_per, bm))) return rc;
+  const size_t bu = static_cast<size_t>(d.nx) * d.nu;
+  for (int p = 0; p < b->B; ++p)
+    for (int t = 0; t < d.T; ++t) {
+      if (A) std::copy_n(a.data() + a_off(d, p, t), d.bsz, A + (static_cast<size_t>(p) * d.T + t) * d.bsz);
+      if (Bm) std::copy_n(bm.data() + b_off(d, p, t), bu, Bm + (static_cast<size_t>(p) * d.T + t) * bu);
+    }
   return DOCP_OK;
 }
 

@@ -55,9 +55,8 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
   double* rd = v.rd + static_cast<long>(p) * T * nu;
   double* lr = v.lr + static_cast<long>(p) * T * nu;
   double* r = v.r + static_cast<long>(p) * T * nu;
-  double* Am = v.A + static_cast<long>(p) * T * bsz;
-  double* Bm = v.Bm + static_cast<long>(p) * T * nx * nu;
   double* Cm = v.C + static_cast<long>(p) * T * nx;
+  const bool tv = d.a_stride != 0;  // time-varying Jacobians stored per stage
   double* xs = v.xs + static_cast<long>(p) * nx;
   if (tid == 0) {
     sh.rank_lin = kNoError;
@@ -118,19 +117,28 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
         lr[t * nu + i] = sqrt(hr);
       }
       double res[kMaxNx];
-      double* jx = Am + static_cast<long>(t) * bsz;
-      double* ju = Bm + static_cast<long>(t) * nx * nu;
-      fam.dynamics(d, th, xn, x, u, res, jx, ju);
+      // time-invariant families: one Jacobian copy, written by stage 0
+      const bool write_jac = tv || t == 0;
+      double* jx = v.A + a_off(d, p, t);
+      double* ju = v.Bm + b_off(d, p, t);
+      fam.dynamics(d, th, xn, x, u, res, write_jac ? jx : nullptr, write_jac ? ju : nullptr);
       bool dfin = true;
       for (int i = 0; i < nx; ++i) dfin = dfin && isfinite(res[i]);
-      for (int k = 0; k < bsz; ++k) dfin = dfin && isfinite(jx[k]);
-      for (int k = 0; k < nx * nu; ++k) dfin = dfin && isfinite(ju[k]);
+      if (write_jac) {
+        for (int k = 0; k < bsz; ++k) dfin = dfin && isfinite(jx[k]);
+        for (int k = 0; k < nx * nu; ++k) dfin = dfin && isfinite(ju[k]);
+      }
       if (!dfin) atomicMin(&sh.rank_lin, T + 2 + 2 * t);
+      // affine-quadratic Jacobians straight from theta (-A, -B: affine_quadratic.hpp:71-72)
+      const double* ath = th + nx + nu;
+      const double* bth = ath + bsz;
+      auto JX = [&](int i, int k) { return write_jac ? jx[i + k * nx] : -ath[i + k * nx]; };
+      auto JU = [&](int i, int k) { return write_jac ? ju[i + k * nx] : -bth[i + k * nx]; };
       for (int i = 0; i < nx; ++i) {  // C_t = A+ x+ + A x + B u - f
-        double ax = jx[i] * x[0];
-        for (int k = 1; k < nx; ++k) ax = ax + jx[i + k * nx] * x[k];
-        double bu = ju[i] * u[0];
-        for (int k = 1; k < nu; ++k) bu = bu + ju[i + k * nx] * u[k];
+        double ax = JX(i, 0) * x[0];
+        for (int k = 1; k < nx; ++k) ax = ax + JX(i, k) * x[k];
+        double bu = JU(i, 0) * u[0];
+        for (int k = 1; k < nu; ++k) bu = bu + JU(i, k) * u[k];
         Cm[t * nx + i] = ((xn[i] + ax) + bu) - res[i];
       }
     } else {  // initial_state (problem.hpp:253-254)
@@ -213,8 +221,6 @@ __global__ void __launch_bounds__(kAsmThreads) assemble_kernel(View v, const int
     }
     const double* lq = v.lq + static_cast<long>(p) * d.nb * nx;
     const double* lr = v.lr + static_cast<long>(p) * T * nu;
-    const double* Am = v.A + static_cast<long>(p) * T * bsz;
-    const double* Bm = v.Bm + static_cast<long>(p) * T * nx * nu;
 
     // ---------------- phase B: chi_t, phi_t, chol(chi_t), chi_t^-1 (schur.hpp:143-167)
     double* blk = blk_ptr(v, p);
@@ -227,8 +233,8 @@ __global__ void __launch_bounds__(kAsmThreads) assemble_kernel(View v, const int
       const double* lqt = lq + t * nx;
       const double* lqn = lq + (t + 1) * nx;
       const double* lrt = lr + t * nu;
-      for (int k = lane; k < bsz; k += 32) sA[k] = Am[static_cast<long>(t) * bsz + k];
-      for (int k = lane; k < nx * nu; k += 32) sB[k] = Bm[static_cast<long>(t) * nx * nu + k];
+      for (int k = lane; k < bsz; k += 32) sA[k] = v.A[a_off(d, p, t) + k];
+      for (int k = lane; k < nx * nu; k += 32) sB[k] = v.Bm[b_off(d, p, t) + k];
       __syncwarp();
       for (int k = lane; k < bsz; k += 32) {
         const int i = k % nx, j = k / nx;
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, co
   static_assert(32 % NX == 0, "group size must divide the warp");
   constexpr int B2 = NX * NX;
   constexpr int BU = NX * NU;
-  constexpr int GBUF = 4 * B2 + 2 * BU;  // doubles of scratch per group
+  constexpr int GBUF = 5 * B2 + 2 * BU;  // doubles of scratch per group
   constexpr int NG = kAsmGroupThreads / NX;
   extern __shared__ double sm_asm[];
   __shared__ AsmShared sh;
@@ -378,6 +384,17 @@ __global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, co
   double* sM2 = sM1 + B2;   // M2
   double* sC = sM2 + BU;    // chi -> X=chi^-1| T1    (phase C)
   double* sD = sC + B2;     // sym(chi)       | P_{t+1} (phase C)
+  double* sO = sD + B2;     // output block staged in the device layout
+  // coalesced copy of the staged block to block b of a region (16-byte stores)
+  auto flush = [&](double* region, int b) {
+    __syncwarp(gmask);
+    double2* dst = reinterpret_cast<double2*>(region + static_cast<long>(b) * B2);
+    const double2* src = reinterpret_cast<const double2*>(sO);
+#pragma unroll
+    for (int k = l; k < B2 / 2; k += NX) dst[k] = src[k];
+    __syncwarp(gmask);
+  };
+  auto stage = [&](int b, int i, int j, double val) { sO[blk_off(NX, b, i, j)] = val; };
 
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
@@ -387,8 +404,6 @@ __global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, co
     }
     const double* lq = v.lq + static_cast<long>(p) * d.nb * NX;
     const double* lr = v.lr + static_cast<long>(p) * T * NU;
-    const double* Am = v.A + static_cast<long>(p) * T * B2;
-    const double* Bm = v.Bm + static_cast<long>(p) * T * BU;
     double* blk = blk_ptr(v, p);
     double* Sd = blk + d.s_diag;
     double* Ss = blk + d.s_sub;
@@ -402,9 +417,9 @@ __global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, co
       const double* lqn = lq + (t + 1) * NX;
       const double* lrt = lr + t * NU;
 #pragma unroll
-      for (int k = l; k < B2; k += NX) sA[k] = Am[static_cast<long>(t) * B2 + k];
+      for (int k = l; k < B2; k += NX) sA[k] = v.A[a_off(d, p, t) + k];
 #pragma unroll
-      for (int k = l; k < BU; k += NX) sB[k] = Bm[static_cast<long>(t) * BU + k];
+      for (int k = l; k < BU; k += NX) sB[k] = v.Bm[b_off(d, p, t) + k];
       __syncwarp(gmask);
       // M1(k, l) = (A(l,k)/lq_k)/lq_k ; M2(k, l) = (B(l,k)/lr_k)/lr_k
 #pragma unroll
@@ -424,17 +439,17 @@ __global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, co
 #pragma unroll
         for (int m = 1; m < NU; ++m) b = b + sB[i + m * NX] * sM2[m + NU * l];
         sC[i + NX * l] = (a + b) + (i == l ? c3 : 0.0);
-        blk_store(Ss, NX, t, i, l, sA[i + l * NX] * dq);
+        stage(t, i, l, sA[i + l * NX] * dq);
       }
-      __syncwarp(gmask);
+      flush(Ss, t);
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
         const double dv = 0.5 * (sC[i + NX * l] + sC[l + NX * i]);
         sD[i + NX * l] = dv;
-        blk_store(Sd, NX, t + 1, i, l, dv);
+        stage(t + 1, i, l, dv);
         sM1[i + NX * l] = 0.0;  // becomes L
       }
-      __syncwarp(gmask);
+      flush(Sd, t + 1);
       // Cholesky of chi_t (eigen_lite LLT): lane l computes row l
       double* sL = sM1;
       bool failed = false;
@@ -499,8 +514,8 @@ __global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, co
       }
       __syncwarp(gmask);
 #pragma unroll
-      for (int i = 0; i < NX; ++i) blk_store(Pd, NX, t + 1, i, l, 0.5 * (sX[i + NX * l] + sX[l + NX * i]));
-      __syncwarp(gmask);
+      for (int i = 0; i < NX; ++i) stage(t + 1, i, l, 0.5 * (sX[i + NX * l] + sX[l + NX * i]));
+      flush(Pd, t + 1);
     }
     __syncthreads();
     if (sh.rank_chi != kNoError) {
@@ -532,9 +547,9 @@ __global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, co
         double a = sC[i] * sD[NX * l];
 #pragma unroll
         for (int m = 1; m < NX; ++m) a = a + sC[i + m * NX] * sD[m + NX * l];
-        blk_store(Pu, NX, t, i, l, a);
+        stage(t, i, l, a);
       }
-      __syncwarp(gmask);
+      flush(Pu, t);
     }
     __syncthreads();
   }
@@ -543,43 +558,56 @@ __global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, co
 /// Solve Q_t x = b for the diagonal Cholesky factor l: (b / l) / l.
 __device__ inline double diag_solve(double b, double l) { return (b / l) / l; }
 
-/// GAMMA <- -(d + H G^-1 b) (schur.hpp:187-211), one thread per (stage, row).
+/// GAMMA <- -(d + H G^-1 b) (schur.hpp:187-211), one CTA per problem: the
+/// block solves Q_t^-1 b_x, R_t^-1 b_u are formed once per entry into SMEM
+/// (two divisions each, as the reference's LLT solves), then every output row
+/// folds them in the reference order.
 /// rhs FORWARD: b = flat_b, d = flat_d; ADJOINT: b = -LOSS_GRAD_Z, d = 0.
 __global__ void gamma_kernel(View v, const int* __restrict__ work, const int* __restrict__ n_work, int rhs) {
+  extern __shared__ double sm_gam[];
   const Dims d = v.d;
   const int nx = d.nx, nu = d.nu, T = d.T;
-  const long total = static_cast<long>(*n_work) * d.nl;
-  for (long g = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; g < total;
-       g += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int p = work[g / d.nl];
-    const int row = static_cast<int>(g % d.nl);
-    const int blk = row / nx, i = row % nx;
+  double* sq = sm_gam;              // [T+1][nx]
+  double* su = sm_gam + d.nb * nx;  // [T][nu]
+  for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
+    const int p = work[w];
     const double* lq = v.lq + static_cast<long>(p) * d.nb * nx;
     const double* lr = v.lr + static_cast<long>(p) * T * nu;
     const double* lg = v.lgz + static_cast<long>(p) * d.nz;
-    auto bx = [&](int t, int k) -> double {
-      return rhs == DOCP_RHS_FORWARD ? v.q[(static_cast<long>(p) * d.nb + t) * nx + k] : -lg[xoff(d, t) + k];
-    };
-    auto bu = [&](int t, int k) -> double {
-      return rhs == DOCP_RHS_FORWARD ? v.r[(static_cast<long>(p) * T + t) * nu + k] : -lg[uoff(d, t) + k];
-    };
-    double out;
-    if (blk == 0) {
-      const double dd = rhs == DOCP_RHS_FORWARD ? v.xs[static_cast<long>(p) * nx + i] : 0.0;
-      out = dd + diag_solve(bx(0, i), lq[i]);
-    } else {
-      const int t = blk - 1;
-      const double* At = v.A + (static_cast<long>(p) * T + t) * d.bsz;
-      const double* Bt = v.Bm + (static_cast<long>(p) * T + t) * nx * nu;
-      double a = At[i] * diag_solve(bx(t, 0), lq[t * nx]);
-      for (int k = 1; k < nx; ++k) a = a + At[i + k * nx] * diag_solve(bx(t, k), lq[t * nx + k]);
-      double b = Bt[i] * diag_solve(bu(t, 0), lr[t * nu]);
-      for (int k = 1; k < nu; ++k) b = b + Bt[i + k * nx] * diag_solve(bu(t, k), lr[t * nu + k]);
-      const double c = diag_solve(bx(t + 1, i), lq[(t + 1) * nx + i]);
-      const double dd = rhs == DOCP_RHS_FORWARD ? v.C[(static_cast<long>(p) * T + t) * nx + i] : 0.0;
-      out = dd + ((a + b) + c);
+    for (int e = threadIdx.x; e < d.nb * nx; e += blockDim.x) {
+      const int t = e / nx, k = e % nx;
+      const double b = rhs == DOCP_RHS_FORWARD ? v.q[static_cast<long>(p) * d.nb * nx + e] : -lg[xoff(d, t) + k];
+      sq[e] = diag_solve(b, lq[e]);
     }
-    v.gamma[static_cast<long>(p) * d.nl + row] = -out;
+    for (int e = threadIdx.x; e < T * nu; e += blockDim.x) {
+      const int t = e / nu, k = e % nu;
+      const double b = rhs == DOCP_RHS_FORWARD ? v.r[static_cast<long>(p) * T * nu + e] : -lg[uoff(d, t) + k];
+      su[e] = diag_solve(b, lr[e]);
+    }
+    __syncthreads();
+    for (int row = threadIdx.x; row < d.nl; row += blockDim.x) {
+      const int blk = row / nx, i = row % nx;
+      double out;
+      if (blk == 0) {
+        const double dd = rhs == DOCP_RHS_FORWARD ? v.xs[static_cast<long>(p) * nx + i] : 0.0;
+        out = dd + sq[i];
+      } else {
+        const int t = blk - 1;
+        const double* At = v.A + a_off(d, p, t);
+        const double* Bt = v.Bm + b_off(d, p, t);
+        const double* s0 = sq + t * nx;
+        const double* s1 = su + t * nu;
+        double a = At[i] * s0[0];
+        for (int k = 1; k < nx; ++k) a = a + At[i + k * nx] * s0[k];
+        double b = Bt[i] * s1[0];
+        for (int k = 1; k < nu; ++k) b = b + Bt[i + k * nx] * s1[k];
+        const double c = sq[(t + 1) * nx + i];
+        const double dd = rhs == DOCP_RHS_FORWARD ? v.C[(static_cast<long>(p) * T + t) * nx + i] : 0.0;
+        out = dd + ((a + b) + c);
+      }
+      v.gamma[static_cast<long>(p) * d.nl + row] = -out;
+    }
+    __syncthreads();
   }
 }
 
@@ -603,7 +631,7 @@ __global__ void recover_kernel(View v, const int* __restrict__ work, const int* 
       if (rhs == DOCP_RHS_FORWARD) rhs_v = v.q[(static_cast<long>(p) * d.nb + t) * nx + i];
       rhs_v = rhs_v + lam[t * nx + i];
       if (t < T) {
-        const double* At = v.A + (static_cast<long>(p) * T + t) * d.bsz;
+        const double* At = v.A + a_off(d, p, t);
         const double* l1 = lam + (t + 1) * nx;
         double a = At[i * nx] * l1[0];
         for (int k = 1; k < nx; ++k) a = a + At[k + i * nx] * l1[k];
@@ -613,7 +641,7 @@ __global__ void recover_kernel(View v, const int* __restrict__ work, const int* 
     } else {  // u_t,i = -R_t^-1 (b + B_t' lam_{t+1})
       const int i = c - nx;
       if (rhs == DOCP_RHS_FORWARD) rhs_v = v.r[(static_cast<long>(p) * T + t) * nu + i];
-      const double* Bt = v.Bm + (static_cast<long>(p) * T + t) * nx * nu;
+      const double* Bt = v.Bm + b_off(d, p, t);
       const double* l1 = lam + (t + 1) * nx;
       double a = Bt[i * nx] * l1[0];
       for (int k = 1; k < nx; ++k) a = a + Bt[k + i * nx] * l1[k];
