@@ -362,7 +362,7 @@ constexpr int kAsmGroupThreads = 128;
 /// chol(chi_t), chi_t^-1 and the stair off-diagonal follow with the same
 /// operation order as the runtime-shape kernel (bit-identical results).
 template <int NX, int NU>
-__global__ void __launch_bounds__(kAsmGroupThreads) assemble_kernel_t(View v, const int* __restrict__ work,
+__global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v, const int* __restrict__ work,
                                                                       const int* __restrict__ n_work, double eps_pd,
                                                                       int do_schur) {
   static_assert(32 % NX == 0, "group size must divide the warp");

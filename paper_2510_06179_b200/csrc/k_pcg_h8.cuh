@@ -138,7 +138,9 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
       s = warp_sum(s);
       if (lane == 0) red[warp] = s;
       __syncthreads();
-      return warp_sum(lane < nw ? red[lane] : 0.0);
+      double t = red[0];  // fixed-order sum of the warp partials, same in every thread
+      for (int k = 1; k < nw; ++k) t = t + red[k];
+      return t;
     } else {
       if (act)
 #pragma unroll
@@ -215,68 +217,65 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
     if (act) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) lam[q] = sol[i * 8 + 4 * h + q];
-      h8::store_half(vbuf, i, h, lam);
     }
     if constexpr (RESIDENT) mbar_wait(&s_bar, phase);
     phase ^= 1;
     __syncthreads();
 
-    // out = A x, x: own half in xr, full vectors in vbuf
+    // out = A x. Phase 1 (no barrier before it): the other half of x_i comes
+    // from the partner lane (lane ^ 1) by shuffle; the thread publishes its
+    // half of x_i (for block row i-1) and its hand-over (for block row i+1),
+    // and forms its diagonal term. One barrier. Phase 2: x_{i+1} and the
+    // hand-over from block row i-1 complete the row (diag, sub, super order).
     auto matvec = [&](bool precond, const double* xr, double* out) {
-      double own[4], up[4], hand[4];
-      if (act) {
-        double xf[8], xn[8];
-        double other[4];
-        h8::load_half(vbuf, i, 1 - h, other);
-        // assemble the full x_i without dynamic indexing (h is 0 or 1)
+      double other[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double a = h ? other[q] : xr[q];
-          const double b = h ? xr[q] : other[q];
-          xf[q] = a;
-          xf[4 + q] = b;
-        }
-        const bool has_next = i + 1 < nb;
-        if (has_next) {
-          h8::load_half(vbuf, i + 1, 0, xn);
-          h8::load_half(vbuf, i + 1, 1, xn + 4);
-        }
-        const double* D = precond ? Pd : Sd;
-        const double* O = precond ? Pu : Ss;
+      for (int q = 0; q < 4; ++q) other[q] = __shfl_xor_sync(0xffffffffu, xr[q], 1);
+      double xf[8], own[4], hand[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        xf[q] = h ? other[q] : xr[q];
+        xf[4 + q] = h ? xr[q] : other[q];
+      }
+      const double* D = precond ? Pd : Sd;
+      const double* O = precond ? Pu : Ss;
+      const bool has_next = i + 1 < nb;
+      if (act) {
+        h8::store_half(vbuf, i, h, xr);
         h8::col_dots<PAR, RESIDENT>(D, i, h, xf, own);
         if (has_next) {
-          if (!precond) {  // -S: up = L_i' x_{i+1} (column dots), hand = L_i x_i (row accumulation)
-            h8::col_dots<PAR, RESIDENT>(O, i, h, xn, up);
-            h8::row_accum<PAR, RESIDENT>(O, i, h, xf, hand);
-          } else {  // Phi^-1: up = U_i x_{i+1} (row accumulation), hand = U_i' x_i (column dots)
-            h8::row_accum<PAR, RESIDENT>(O, i, h, xn, up);
-            h8::col_dots<PAR, RESIDENT>(O, i, h, xf, hand);
-          }
+          if (!precond) h8::row_accum<PAR, RESIDENT>(O, i, h, xf, hand);  // L_i x_i
+          else h8::col_dots<PAR, RESIDENT>(O, i, h, xf, hand);            // U_i' x_i
           h8::store_half(xbuf, i, h, hand);
         }
       }
       __syncthreads();
       if (act) {
-        double low[4];
+        double up[4], low[4];
+        if (has_next) {
+          double xn[8];
+          h8::load_half(vbuf, i + 1, 0, xn);
+          h8::load_half(vbuf, i + 1, 1, xn + 4);
+          if (!precond) h8::col_dots<PAR, RESIDENT>(O, i, h, xn, up);  // L_i' x_{i+1}
+          else h8::row_accum<PAR, RESIDENT>(O, i, h, xn, up);          // U_i x_{i+1}
+        }
         if (i > 0) h8::load_half(xbuf, i - 1, h, low);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           double acc = own[q];
           if (i > 0) acc = acc + low[q];
-          if (i + 1 < nb) acc = acc + up[q];
+          if (has_next) acc = acc + up[q];
           out[q] = acc;
         }
       }
     };
 
-    matvec(false, lam, y);
+    matvec(false, lam, y);  // y = (-S) lambda0
     if (act)
 #pragma unroll
       for (int q = 0; q < 4; ++q) r[q] = gam[i * 8 + 4 * h + q] - y[q];
-    __syncthreads();
-    if (act) h8::store_half(vbuf, i, h, r);
-    __syncthreads();
-    matvec(true, r, pv);
+    __syncthreads();  // every phase-2 read of lambda / its hand-over is done
+    matvec(true, r, pv);  // r~
     double eta = dot(r, pv);
     int status = DOCP_OK, iters = 0;
     if (eta < 0.0) {
@@ -284,10 +283,8 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
       if (-eta <= 1e-10 * scale + 1e-300) eta = 0.0;
       else status = DOCP_AT_PCG_PRECOND;
     }
-    if (act) h8::store_half(vbuf, i, h, pv);
 
     while (status == DOCP_OK && eta > threshold && iters < max_iters) {
-      __syncthreads();
       matvec(false, pv, y);
       const double vv = dot(pv, y);
       if (vv <= 0.0) {
@@ -306,10 +303,8 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
             r[q] = fma(-alpha, y[q], r[q]);
           }
         }
-        h8::store_half(vbuf, i, h, r);
       }
-      __syncthreads();
-      matvec(true, r, y);
+      matvec(true, r, y);  // r~ (y reused)
       double eta_next = dot(r, y);
       if (eta_next < 0.0) {
         const double scale = norm(r) * norm(y);
@@ -327,7 +322,6 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
           if constexpr (PAR) pv[q] = y[q] + beta * pv[q];
           else pv[q] = fma(beta, pv[q], y[q]);
         }
-        h8::store_half(vbuf, i, h, pv);
       }
       eta = eta_next;
       ++iters;
