@@ -46,15 +46,17 @@ __host__ __device__ inline int uoff(const Dims& d, int t) { return t * (d.nx + d
 /// column and the columns are permuted per block index b so that the PCG
 /// kernels' shared-memory reads are bank-conflict free (each quarter-warp
 /// LDS.128 touches 8 distinct 4-bank groups):
-///   NX = 8: s' = s ^ (b & 1),   chunk' = chunk ^ (b & 3)
-///           (pcg_kernel_h8: two threads per block row; see its access orders)
+///   NX = 8: s' = s ^ (b & 1),   chunk' = chunk ^ ((b >> 1) & 1) ^ (2 * ((s >> 2) & 1))
+///           (pcg_kernel_h8: two threads per block row reading row halves
+///            (chunks 2h, 2h+1 of every column) or column halves)
 ///   NX = 4: s' = s ^ (b & 3),   chunk' = chunk ^ ((b >> 2) & 1)
 ///           (pcg_kernel: one thread per block row)
 ///   other : plain column-major.
 __host__ __device__ inline int blk_off(int nx, int b, int e, int s) {
   if (nx == 8) {
     const int sp = s ^ (b & 1);
-    return sp * 8 + ((((e >> 1) ^ (b & 3)) << 1) | (e & 1));
+    const int ch = (e >> 1) ^ ((b >> 1) & 1) ^ (((s >> 2) & 1) << 1);
+    return sp * 8 + ((ch << 1) | (e & 1));
   }
   if (nx == 4) {
     const int sp = s ^ (b & 3);

@@ -36,20 +36,26 @@ __device__ __forceinline__ void col8(const double* region, int b, int s, double*
 /// out[q] = dot(column 4h+q of block b, X) for q = 0..3 (left folds).
 template <bool PAR, bool SMEM>
 __device__ __forceinline__ void col_dots(const double* region, int b, int h, const double* X, double* out) {
-  double t[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     double m[8];
-    col8<SMEM>(region, b, 4 * h + ((j + h) & 3), m);
+    col8<SMEM>(region, b, 4 * h + j, m);
     double a = m[0] * X[0];
 #pragma unroll
     for (int e = 1; e < 8; ++e) a = madd<PAR>(m[e], X[e], a);
-    t[j] = a;
+    out[j] = a;
   }
-  out[0] = h ? t[3] : t[0];
-  out[1] = h ? t[0] : t[1];
-  out[2] = h ? t[1] : t[2];
-  out[3] = h ? t[2] : t[3];
+}
+
+/// Rows 4h..4h+3 of block b: half[c] = (B(4h,c), B(4h+1,c), B(4h+2,c), B(4h+3,c)).
+template <bool SMEM>
+__device__ __forceinline__ void row_half(const double* region, int b, int h, double2 (&lo)[8], double2 (&hi)[8]) {
+  const double* base = region + static_cast<long>(b) * 64;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    lo[c] = ld2<SMEM>(base + blk_off(8, b, 4 * h, c));
+    hi[c] = ld2<SMEM>(base + blk_off(8, b, 4 * h + 2, c));
+  }
 }
 
 /// out[q] = sum_c B(4h+q, c) Y[c] for q = 0..3, c ascending (left folds).
@@ -58,10 +64,8 @@ __device__ __forceinline__ void row_accum(const double* region, int b, int h, co
   const double* base = region + static_cast<long>(b) * 64;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const double2 d0 = ld2<SMEM>(base + blk_off(8, b, 2 * (2 * h + h), c));
-    const double2 d1 = ld2<SMEM>(base + blk_off(8, b, 2 * (2 * h + (1 - h)), c));
-    const double2 lo = h ? d1 : d0;  // rows 4h, 4h+1
-    const double2 hi = h ? d0 : d1;  // rows 4h+2, 4h+3
+    const double2 lo = ld2<SMEM>(base + blk_off(8, b, 4 * h, c));      // rows 4h, 4h+1
+    const double2 hi = ld2<SMEM>(base + blk_off(8, b, 4 * h + 2, c));  // rows 4h+2, 4h+3
     if (c == 0) {
       out[0] = lo.x * Y[0];
       out[1] = lo.y * Y[0];
@@ -270,12 +274,117 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
       }
     };
 
-    matvec(false, lam, y);  // y = (-S) lambda0
+    // FAST product: each thread reads only its row half (rows 4h..4h+3) of
+    // D_i and O_i — O_i once, kept in registers across the barrier — and
+    // forms the transposed product (L_i' x_{i+1}, resp. U_i' x_i) from
+    // half-column partial sums exchanged with the partner lane.
+    auto matvec_fast = [&](bool precond, const double* xr, double* out) {
+      double other[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) other[q] = __shfl_xor_sync(0xffffffffu, xr[q], 1);
+      double xf[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        xf[q] = h ? other[q] : xr[q];
+        xf[4 + q] = h ? xr[q] : other[q];
+      }
+      const double* D = precond ? Pd : Sd;
+      const double* O = precond ? Pu : Ss;
+      const bool has_next = act && i + 1 < nb;
+      const int bo = has_next ? i : 0;  // O_i exists only below the last block row
+      double own[4] = {0, 0, 0, 0}, hand[4] = {0, 0, 0, 0};
+      double2 olo[8] = {}, ohi[8] = {};
+      if (act) {
+        h8::store_half(vbuf, i, h, xr);
+        double2 dlo[8], dhi[8];
+        h8::row_half<RESIDENT>(D, i, h, dlo, dhi);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          own[0] = fma(dlo[c].x, xf[c], own[0]);
+          own[1] = fma(dlo[c].y, xf[c], own[1]);
+          own[2] = fma(dhi[c].x, xf[c], own[2]);
+          own[3] = fma(dhi[c].y, xf[c], own[3]);
+        }
+      }
+      if (has_next) h8::row_half<RESIDENT>(O, bo, h, olo, ohi);
+      double part[8];  // half-column partial sums over my rows (P: with x_i)
+      if (precond) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          double a = olo[c].x * xr[0];
+          a = fma(olo[c].y, xr[1], a);
+          a = fma(ohi[c].x, xr[2], a);
+          part[c] = fma(ohi[c].y, xr[3], a);
+        }
+        double recv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) recv[q] = __shfl_xor_sync(0xffffffffu, h ? part[q] : part[4 + q], 1);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) hand[q] = (h ? part[4 + q] : part[q]) + recv[q];  // U_i' x_i
+      } else if (has_next) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // L_i x_i, my rows
+          hand[0] = fma(olo[c].x, xf[c], hand[0]);
+          hand[1] = fma(olo[c].y, xf[c], hand[1]);
+          hand[2] = fma(ohi[c].x, xf[c], hand[2]);
+          hand[3] = fma(ohi[c].y, xf[c], hand[3]);
+        }
+      }
+      if (has_next) h8::store_half(xbuf, i, h, hand);
+      __syncthreads();
+      double xn[8];
+      if (has_next) {
+        h8::load_half(vbuf, i + 1, 0, xn);
+        h8::load_half(vbuf, i + 1, 1, xn + 4);
+        h8::row_half<RESIDENT>(O, bo, h, olo, ohi);  // re-read: cheaper than 64 live registers
+      }
+      double up[4] = {0, 0, 0, 0};
+      if (!precond) {  // L_i' x_{i+1}: partial sums over my rows of x_{i+1}
+        const double* xh = h ? xn + 4 : xn;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          double a = olo[c].x * xh[0];
+          a = fma(olo[c].y, xh[1], a);
+          a = fma(ohi[c].x, xh[2], a);
+          part[c] = fma(ohi[c].y, xh[3], a);
+        }
+        double recv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) recv[q] = __shfl_xor_sync(0xffffffffu, h ? part[q] : part[4 + q], 1);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) up[q] = (h ? part[4 + q] : part[q]) + recv[q];
+      } else if (has_next) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // U_i x_{i+1}, my rows
+          up[0] = fma(olo[c].x, xn[c], up[0]);
+          up[1] = fma(olo[c].y, xn[c], up[1]);
+          up[2] = fma(ohi[c].x, xn[c], up[2]);
+          up[3] = fma(ohi[c].y, xn[c], up[3]);
+        }
+      }
+      if (act) {
+        double low[4];
+        if (i > 0) h8::load_half(xbuf, i - 1, h, low);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double acc = own[q];
+          if (i > 0) acc = acc + low[q];
+          if (has_next) acc = acc + up[q];
+          out[q] = acc;
+        }
+      }
+    };
+    auto mv = [&](bool precond, const double* xr, double* out) {
+      if constexpr (PAR) matvec(precond, xr, out);
+      else matvec_fast(precond, xr, out);
+    };
+
+    mv(false, lam, y);  // y = (-S) lambda0
     if (act)
 #pragma unroll
       for (int q = 0; q < 4; ++q) r[q] = gam[i * 8 + 4 * h + q] - y[q];
     __syncthreads();  // every phase-2 read of lambda / its hand-over is done
-    matvec(true, r, pv);  // r~
+    mv(true, r, pv);  // r~
     double eta = dot(r, pv);
     int status = DOCP_OK, iters = 0;
     if (eta < 0.0) {
@@ -285,7 +394,7 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
     }
 
     while (status == DOCP_OK && eta > threshold && iters < max_iters) {
-      matvec(false, pv, y);
+      mv(false, pv, y);
       const double vv = dot(pv, y);
       if (vv <= 0.0) {
         status = DOCP_AT_PCG_CURVATURE;
@@ -304,7 +413,7 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
           }
         }
       }
-      matvec(true, r, y);  // r~ (y reused)
+      mv(true, r, y);  // r~ (y reused)
       double eta_next = dot(r, y);
       if (eta_next < 0.0) {
         const double scale = norm(r) * norm(y);
