@@ -306,6 +306,9 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
           own[3] = fma(dhi[c].y, xf[c], own[3]);
         }
       }
+      // D's loads are consumed above; keep the compiler from hoisting O's
+      // loads over them (bounds the live registers: O stays resident, D does not)
+      asm volatile("" ::: "memory");
       if (has_next) h8::row_half<RESIDENT>(O, bo, h, olo, ohi);
       double part[8];  // half-column partial sums over my rows (P: with x_i)
       if (precond) {
@@ -336,7 +339,6 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
       if (has_next) {
         h8::load_half(vbuf, i + 1, 0, xn);
         h8::load_half(vbuf, i + 1, 1, xn + 4);
-        h8::row_half<RESIDENT>(O, bo, h, olo, ohi);  // re-read: cheaper than 64 live registers
       }
       double up[4] = {0, 0, 0, 0};
       if (!precond) {  // L_i' x_{i+1}: partial sums over my rows of x_{i+1}
