@@ -63,22 +63,28 @@ int ensure_hist(docp_batch* b, int n) {
 
 // ---------------------------------------------------------------- kernels of the driver
 __global__ void init_solve_kernel(View v, int* __restrict__ list, int* __restrict__ count) {
+  // one warp per problem: coalesced finiteness scan of z0 and lambda0 (sqp.hpp:217-224)
   const Dims d = v.d;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < v.B; p += gridDim.x * blockDim.x) {
-    bool fin = true;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < v.B; p += warps) {
     const double* z = v.z + static_cast<long>(p) * d.nz;
     const double* l = v.lam + static_cast<long>(p) * d.nl;
-    for (int e = 0; e < d.nz; ++e) fin = fin && isfinite(z[e]);
-    for (int e = 0; e < d.nl; ++e) fin = fin && isfinite(l[e]);
-    v.mu[p] = 1.0;
-    v.sqp_iters[p] = 0;
-    v.converged[p] = 0;
-    v.kkt[p] = 0.0;
-    if (fin) {
-      set_status(v.status + p, DOCP_OK, DOCP_AT_NONE, 0);
-      list[atomicAdd(count, 1)] = p;
-    } else {
-      set_status(v.status + p, DOCP_DIMENSION, DOCP_AT_INITIAL_GUESS, 0);
+    bool fin = true;
+    for (int e = lane; e < d.nz; e += 32) fin = fin && isfinite(z[e]);
+    for (int e = lane; e < d.nl; e += 32) fin = fin && isfinite(l[e]);
+    fin = __all_sync(0xffffffffu, fin);
+    if (lane == 0) {
+      v.mu[p] = 1.0;
+      v.sqp_iters[p] = 0;
+      v.converged[p] = 0;
+      v.kkt[p] = 0.0;
+      if (fin) {
+        set_status(v.status + p, DOCP_OK, DOCP_AT_NONE, 0);
+        list[atomicAdd(count, 1)] = p;
+      } else {
+        set_status(v.status + p, DOCP_DIMENSION, DOCP_AT_INITIAL_GUESS, 0);
+      }
     }
   }
 }
@@ -575,7 +581,7 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
   if ((rc = ensure_hist(b, std::max(1, cfg->max_sqp_iters)))) return rc;
   int cur = 0;
   CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, 2 * sizeof(int), b->stream));
-  init_solve_kernel<<<grid_for(b->B, 128, 4096), 128, 0, b->stream>>>(b->v, b->list[0], b->counts + 1);
+  init_solve_kernel<<<grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8), 256, 0, b->stream>>>(b->v, b->list[0], b->counts + 1);
   LAUNCH_CHECK();
   int n_active = 0;
   if ((rc = read_count(b, b->counts + 1, &n_active))) return rc;
@@ -634,11 +640,17 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
                     b->stream>>>(b->v, weights, learn_start, learn_size, demos);
   LAUNCH_CHECK();
   if ((rc = docp_sqp_solve(b, cfg))) return rc;
-  il_loss_kernel<<<grid_for(b->B, 128, 4096), 128, 0, b->stream>>>(b->v, demos, den);
+  il_loss_kernel<<<grid_for(static_cast<long>(b->B) * 32, kIlLossThreads, b->num_sms * 8), kIlLossThreads, 0, b->stream>>>(b->v, demos, den);
   LAUNCH_CHECK();
   if ((rc = docp_backward_vjp(b, &cfg->pcg))) return rc;
-  il_sum_kernel<<<grid_for(learn_size + 1, 64, 64), 64, 0, b->stream>>>(b->v, learn_start, learn_size, loss_sum,
-                                                                         grad_sum);
+  {
+    const int cols = 1 + learn_size;
+    const int ctas = (cols + kIlSumThreads - 1) / kIlSumThreads;
+    const int ncol = std::min(kIlSumThreads, cols);
+    const int rows = std::max(1, std::min(1024, (40 * 1024 / 8) / ncol));
+    il_sum_kernel<<<ctas, kIlSumThreads, static_cast<size_t>(rows) * ncol * sizeof(double), b->stream>>>(
+        b->v, learn_start, learn_size, rows, loss_sum, grad_sum);
+  }
   LAUNCH_CHECK();
   return DOCP_OK;
 }

@@ -358,40 +358,80 @@ __global__ void il_setup_kernel(View v, const double* __restrict__ weights, int 
 }
 
 /// IL epoch, after the solve: loss_j = |u - u^|^2 / den and its gradient in
-/// the flat layout (train.hpp:89-95), one thread per problem.
-__global__ void il_loss_kernel(View v, const double* __restrict__ demos, double den) {
+/// the flat layout (train.hpp:89-95). One warp per problem: the gradient row
+/// is written coalesced, the squared control errors are staged in shared
+/// memory and lane 0 folds them in (t, i) order, as the reference does.
+constexpr int kIlLossThreads = 256;
+constexpr int kIlLossChunk = 256;  // staged squares per warp per pass
+__global__ void __launch_bounds__(kIlLossThreads) il_loss_kernel(View v, const double* __restrict__ demos, double den) {
+  __shared__ double sq[kIlLossThreads / 32][kIlLossChunk];
   const Dims d = v.d;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < v.B; p += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int stage = d.nx + d.nu;
+  const int nu_tot = d.T * d.nu;
+  const double g2 = 2.0 / den;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < v.B; p += warps) {
     const double* z = v.z + static_cast<long>(p) * d.nz;
     const double* dm = demos + static_cast<long>(p) * d.nz;
     double* lg = v.lgz + static_cast<long>(p) * d.nz;
     double acc = 0.0;
-    bool first = true;
-    for (int e = 0; e < d.nz; ++e) lg[e] = 0.0;
-    for (int t = 0; t < d.T; ++t)
-      for (int i = 0; i < d.nu; ++i) {
-        const double du = z[uoff(d, t) + i] - dm[uoff(d, t) + i];
-        acc = first ? du * du : acc + du * du;
-        first = false;
-        lg[uoff(d, t) + i] = 2.0 / den * du;
+    for (int base = 0; base < d.nz; base += kIlLossChunk / d.nu * stage) {
+      // this pass covers stages [base/stage, base/stage + kIlLossChunk/nu)
+      const int end = min(d.nz, base + kIlLossChunk / d.nu * stage);
+      for (int e = base + lane; e < end; e += 32) {
+        const int t = e / stage, r = e - t * stage;
+        double gv = 0.0;
+        if (r >= d.nx && t < d.T) {
+          const double du = z[e] - dm[e];
+          sq[w][(t * d.nu + r - d.nx) - (base / stage) * d.nu] = du * du;
+          gv = g2 * du;
+        }
+        lg[e] = gv;
       }
-    v.loss[p] = acc / den;
+      __syncwarp();
+      if (lane == 0) {
+        const int k0 = (base / stage) * d.nu;
+        const int k1 = min(nu_tot, k0 + kIlLossChunk);
+        for (int k = k0; k < k1; ++k) acc = (k == 0) ? sq[w][0] : acc + sq[w][k - k0];
+      }
+      __syncwarp();
+    }
+    if (lane == 0) v.loss[p] = acc / den;
   }
 }
 
-/// Fixed-order (instance order) sums of the epoch (train.hpp:126-131):
-/// thread 0 sums the losses, thread 1+k the k-th learnable gradient entry.
-__global__ void il_sum_kernel(View v, int learn_start, int learn_size, double* __restrict__ loss_sum,
-                              double* __restrict__ grad_sum) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k == 0) {
-    double acc = 0.0;
-    for (int p = 0; p < v.B; ++p) acc = acc + v.loss[p];
-    *loss_sum = acc;
-  } else if (k - 1 < learn_size) {
-    double acc = 0.0;
-    for (int p = 0; p < v.B; ++p) acc = acc + v.grad[static_cast<long>(p) * v.d.nth + learn_start + k - 1];
-    grad_sum[k - 1] = acc;
+/// Fixed-order (instance order) sums of the epoch (train.hpp:126-131). Column
+/// 0 is the loss, column 1 + i the i-th learnable gradient entry; CTA c owns
+/// columns [c * kIlSumThreads, ...). It stages `rows` instances of its columns
+/// in shared memory (coalesced, all loads in flight), then thread k folds its
+/// column in instance order.
+constexpr int kIlSumThreads = 256;
+__global__ void __launch_bounds__(kIlSumThreads) il_sum_kernel(View v, int learn_start, int learn_size, int rows,
+                                                               double* __restrict__ loss_sum,
+                                                               double* __restrict__ grad_sum) {
+  extern __shared__ double stage_buf[];  // [rows][ncol]
+  const int c0 = blockIdx.x * kIlSumThreads;
+  const int ncol = min(kIlSumThreads, 1 + learn_size - c0);
+  const int k = threadIdx.x;
+  double acc = 0.0;
+  for (int p0 = 0; p0 < v.B; p0 += rows) {
+    const int n = min(rows, v.B - p0);
+    __syncthreads();
+    for (int g = threadIdx.x; g < n * ncol; g += blockDim.x) {
+      const int j = g / ncol, c = c0 + (g - j * ncol);
+      const long p = p0 + j;
+      stage_buf[g] = c == 0 ? v.loss[p] : v.grad[p * v.d.nth + learn_start + c - 1];
+    }
+    __syncthreads();
+    if (k < ncol) {
+#pragma unroll 8
+      for (int j = 0; j < n; ++j) acc = acc + stage_buf[j * ncol + k];
+    }
+  }
+  if (k < ncol) {
+    if (c0 + k == 0) *loss_sum = acc;
+    else grad_sum[c0 + k - 1] = acc;
   }
 }
 
