@@ -5,6 +5,8 @@
   oracle/_build/libdocp_port.so               C restatement (test checker)
   oracle/_ref/*                               reference headers + eigen_lite
                                               (only where /root/reference exists)
+  tests/cpp/_bin/test_dropin                  C++ drop-in tests (docp_gpu.hpp vs the
+                                              reference headers; same condition)
 """
 import os
 import subprocess
@@ -65,6 +67,7 @@ def build_oracle():
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"], check=True)
     if os.path.isdir("/root/reference/proj/include"):
         subprocess.run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
 
 
 def main():
