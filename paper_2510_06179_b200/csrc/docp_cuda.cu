@@ -210,20 +210,40 @@ int launch_step(docp_batch* b, const docp_sqp_config& cfg, const int* list, cons
   sc.iter = iter;
   sc.max_iters = cfg.max_sqp_iters;
   sc.is_loop = is_loop;
-  const int T = b->d.T;
-  const size_t smem = (static_cast<size_t>(sc.n_alpha + 1) * (3 * T + 2) + 2 * (2 * T + 1)) * sizeof(double);
-  CUDA_TRY(cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  if (smem > 200 * 1024) return fail(DOCP_UNSUPPORTED, "line search: horizon too long");
-  const int grid = std::max(1, std::min(n_hint, b->num_sms * 8));
+  const size_t smem = static_cast<size_t>(step_smem_doubles(b->d, sc.n_alpha)) * sizeof(double);
+  int max_optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device));
+  if (smem + 1024 > static_cast<size_t>(max_optin)) return fail(DOCP_UNSUPPORTED, "line search: horizon too long");
+  auto kern = step_kernel<0, 0>;
+  const int nx = b->d.nx, nu = b->d.nu;
+  if (nx == 8 && nu == 4) kern = step_kernel<8, 4>;
+  else if (nx == 8 && nu == 2) kern = step_kernel<8, 2>;
+  else if (nx == 4 && nu == 2) kern = step_kernel<4, 2>;
+  else if (nx == 4 && nu == 1) kern = step_kernel<4, 1>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem));
+  const int grid = std::max(1, std::min(n_hint, std::max(1, per_sm) * b->num_sms));
   ProfScope ps(b, DOCP_PROF_STEP);
-  step_kernel<<<grid, kStepThreads, smem, b->stream>>>(b->v, list, count, sc);
+  kern<<<grid, kStepThreads, smem, b->stream>>>(b->v, list, count, sc);
   LAUNCH_CHECK();
   return DOCP_OK;
 }
 
 int launch_kkt(docp_batch* b, const int* list, const int* count, int n_hint) {
+  const size_t smem = static_cast<size_t>(b->d.nz + b->d.nl + b->d.nth) * sizeof(double);
+  auto kern = kkt_kernel<0, 0>;
+  const int nx = b->d.nx, nu = b->d.nu;
+  if (nx == 8 && nu == 4) kern = kkt_kernel<8, 4>;
+  else if (nx == 8 && nu == 2) kern = kkt_kernel<8, 2>;
+  else if (nx == 4 && nu == 2) kern = kkt_kernel<4, 2>;
+  else if (nx == 4 && nu == 1) kern = kkt_kernel<4, 1>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kKktThreads, smem));
+  const int grid = std::max(1, std::min(n_hint, std::max(1, per_sm) * b->num_sms));
   ProfScope ps(b, DOCP_PROF_KKT);
-  kkt_kernel<<<std::max(1, std::min(n_hint, b->num_sms * 8)), 64, 0, b->stream>>>(b->v, list, count);
+  kern<<<grid, kKktThreads, smem, b->stream>>>(b->v, list, count);
   LAUNCH_CHECK();
   return DOCP_OK;
 }

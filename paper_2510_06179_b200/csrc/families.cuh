@@ -15,8 +15,11 @@ namespace docp_dev {
 /// Diagonal quadratic stage cost  scale * v' diag(w) v
 /// (affine_quadratic.hpp:47-64, quadratic_cost.hpp:9-20). Returns the value;
 /// grad_i = ((2 scale) w_i) v_i and hess = diag((2 scale) w_i).
-__device__ inline double diag_cost_value(double scale, const double* w, const double* v, int n) {
+template <int N = 0>
+__device__ inline double diag_cost_value(double scale, const double* w, const double* v, int n_rt) {
+  const int n = N ? N : n_rt;
   double acc = v[0] * (w[0] * v[0]);
+#pragma unroll
   for (int i = 1; i < n; ++i) acc = acc + v[i] * (w[i] * v[i]);
   return scale * acc;
 }
@@ -49,18 +52,23 @@ struct Family {
   }
 
   /// Dynamics residual f = x+ - phi(x, u) and its Jacobians (jac_x_next = I).
-  /// res[nx]; jx[nx*nx], ju[nx*nu] column-major (may be null).
+  /// res[nx]; jx[nx*nx], ju[nx*nu] column-major (may be null). NX, NU > 0
+  /// fix the sizes at compile time (same arithmetic, unrolled).
+  template <int NX = 0, int NU = 0>
   __device__ void dynamics(const Dims& d, const double* th, const double* xn, const double* x, const double* u,
                            double* res, double* jx, double* ju) const {
-    const int nx = d.nx, nu = d.nu;
+    const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu;
     if (kind == DOCP_AFFINE_QUADRATIC) {  // affine_quadratic.hpp:65-75
       const double* a = th + nx + nu;
       const double* b = a + nx * nx;
       const double* off = b + nx * nu;
+#pragma unroll
       for (int i = 0; i < nx; ++i) {
         double ax = a[i] * x[0];
+#pragma unroll
         for (int k = 1; k < nx; ++k) ax = ax + a[i + k * nx] * x[k];
         double bu = b[i] * u[0];
+#pragma unroll
         for (int k = 1; k < nu; ++k) bu = bu + b[i + k * nx] * u[k];
         res[i] = ((xn[i] - ax) - bu) - off[i];
       }

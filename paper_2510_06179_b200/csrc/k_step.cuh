@@ -31,64 +31,78 @@ struct StepCfg {
 
 /// Stage terms of merit_parts at one trajectory version (old or a trial).
 /// Slots: state value t -> t, control value t -> T+1+t, dynamics |res|_1
-/// t -> 2T+1+t, initial-condition |x_0 - x_s|_1 -> 3T+1.
+/// t -> 2T+1+t, initial-condition |x_0 - x_s|_1 -> 3T+1. zo, zq, th are the
+/// problem's shared-memory copies; a non-finite cost value lowers *first_bad
+/// to its slot (merit_parts throws at the first one in slot order).
+template <int NX, int NU>
 __device__ inline void merit_task(const Dims& d, const Family& fam, const double* th, const double* zo,
-                                  const double* zq, double alpha, bool trial, int task, double* slots) {
-  const int nx = d.nx, nu = d.nu, T = d.T;
-  double a[kMaxNx], b[kMaxNx], c[kMaxNx], res[kMaxNx];
+                                  const double* zq, double alpha, bool trial, int task, double* slots,
+                                  int* first_bad) {
+  const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T;
+  constexpr int AX = NX ? NX : kMaxNx, AU = NU ? NU : kMaxNx;
+  double a[AX], b[AU], c[AX], res[AX];
   auto get = [&](int off, int n, double* out) {
-    for (int i = 0; i < n; ++i)
-      out[i] = trial ? zo[off + i] + alpha * (zq[off + i] - zo[off + i]) : zo[off + i];
+#pragma unroll
+    for (int i = 0; i < (NX ? (NX > NU ? NX : NU) : kMaxNx); ++i)
+      if (i < n) out[i] = trial ? zo[off + i] + alpha * (zq[off + i] - zo[off + i]) : zo[off + i];
   };
   if (task <= T) {
     get(xoff(d, task), nx, a);
-    slots[task] = diag_cost_value(fam.scale, fam.w_x(d, th), a, nx);
+    const double val = diag_cost_value<NX>(fam.scale, fam.w_x(d, th), a, nx);
+    slots[task] = val;
+    if (!isfinite(val)) atomicMin(first_bad, task);
   } else if (task < 2 * T + 1) {
     const int t = task - (T + 1);
     get(xoff(d, t), nx, a);
     get(uoff(d, t), nu, b);
     get(xoff(d, t + 1), nx, c);
-    slots[T + 1 + t] = diag_cost_value(fam.scale, fam.w_u(d, th), b, nu);
-    fam.dynamics(d, th, c, a, b, res, nullptr, nullptr);
+    const double val = diag_cost_value<NU>(fam.scale, fam.w_u(d, th), b, nu);
+    slots[T + 1 + t] = val;
+    if (!isfinite(val)) atomicMin(first_bad, T + 1 + t);
+    fam.dynamics<NX, NU>(d, th, c, a, b, res, nullptr, nullptr);
     double s = fabs(res[0]);
+#pragma unroll
     for (int i = 1; i < nx; ++i) s = s + fabs(res[i]);
     slots[2 * T + 1 + t] = s;
   } else {
     get(xoff(d, 0), nx, a);
     const double* x_s = fam.x_s(d, th);
     double s = fabs(a[0] - x_s[0]);
+#pragma unroll
     for (int i = 1; i < nx; ++i) s = s + fabs(a[i] - x_s[i]);
     slots[3 * T + 1] = s;
   }
 }
 
-/// Folds one version's slots in merit_parts order; returns false (and the
-/// first failing slot) when a cost value is non-finite.
-__device__ inline bool merit_fold(const Dims& d, const double* slots, double* cost, double* viol, int* bad_slot) {
+/// Folds one version's slots in merit_parts order (sqp.hpp:102-121). Only
+/// called when every cost slot is finite.
+__device__ inline void merit_fold(const Dims& d, const double* slots, double* cost, double* viol) {
   const int T = d.T;
   double c = 0.0, v = 0.0;
-  for (int t = 0; t <= T; ++t) {
-    if (!isfinite(slots[t])) {
-      *bad_slot = t;
-      return false;
-    }
-    c = c + slots[t];
-  }
+#pragma unroll 4
+  for (int t = 0; t <= T; ++t) c = c + slots[t];
+#pragma unroll 4
   for (int t = 0; t < T; ++t) {
-    if (!isfinite(slots[T + 1 + t])) {
-      *bad_slot = T + 1 + t;
-      return false;
-    }
     c = c + slots[T + 1 + t];
     v = v + slots[2 * T + 1 + t];
   }
   v = v + slots[3 * T + 1];
   *cost = c;
   *viol = v;
-  return true;
 }
 
-/// K3: line search from Z toward Z_QP and the SQP-loop bookkeeping.
+/// Dynamic shared memory of step_kernel (doubles): z_old, z_qp, theta, the
+/// merit slots of every version and the d_cost / curvature stage terms.
+__host__ __device__ inline long step_smem_doubles(const Dims& d, int n_alpha) {
+  return 2L * d.nz + d.nth + static_cast<long>(n_alpha + 1) * (3 * d.T + 2) + 2L * (2 * d.T + 1);
+}
+
+/// K3: line search from Z toward Z_QP and the SQP-loop bookkeeping
+/// (sqp.hpp:151-206, 236-251). One CTA per problem: the problem's z_old,
+/// z_qp and theta are staged in shared memory, the stage terms of every
+/// version are evaluated in parallel, and each sum is folded by one thread
+/// in the reference's order. NX, NU > 0 fix the block sizes at compile time.
+template <int NX, int NU>
 __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* __restrict__ work,
                                                            const int* __restrict__ n_work, StepCfg cfg) {
   extern __shared__ double sm_step[];
@@ -97,21 +111,33 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
   __shared__ int s_bad[DOCP_MAX_STEP_CANDIDATES + 1];
   __shared__ int s_nonfinite, s_accepted;
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, T = d.T;
+  const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T;
   const Family fam = Family::from(v.prob);
   const int tid = threadIdx.x;
   const int nslot = 3 * T + 2;
   const int nver = cfg.n_alpha + 1;
-  double* slots = sm_step;                          // [nver][nslot]
+  double* szo = sm_step;                                   // [nz]
+  double* szq = szo + d.nz;                                // [nz]
+  double* sth = szq + d.nz;                                // [nth]
+  double* slots = sth + d.nth;                             // [nver][nslot]
   double* dterm = slots + static_cast<long>(nver) * nslot;  // [2T+1] d_cost terms
-  double* cterm = dterm + 2 * T + 1;                 // [2T+1] curvature terms
+  double* cterm = dterm + 2 * T + 1;                       // [2T+1] curvature terms
 
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
     if (v.status[p].code != DOCP_OK) continue;
-    const double* th = v.theta + static_cast<long>(p) * d.nth;
     double* zo = v.z + static_cast<long>(p) * d.nz;
-    const double* zq = v.zqp + static_cast<long>(p) * d.nz;
+    {
+      const double* th = v.theta + static_cast<long>(p) * d.nth;
+      const double* zq = v.zqp + static_cast<long>(p) * d.nz;
+      for (int e = tid; e < d.nz; e += blockDim.x) {
+        szo[e] = zo[e];
+        szq[e] = zq[e];
+      }
+      for (int e = tid; e < d.nth; e += blockDim.x) sth[e] = th[e];
+      if (tid < nver) s_bad[tid] = 0x7fffffff;
+    }
+    __syncthreads();
     const double* qd = v.qd + static_cast<long>(p) * d.nb * nx;
     const double* rd = v.rd + static_cast<long>(p) * T * nu;
 
@@ -122,12 +148,12 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
       const int s = st ? t : t - (T + 1);
       const int n = st ? nx : nu;
       const int off = st ? xoff(d, s) : uoff(d, s);
-      const double* w = st ? fam.w_x(d, th) : fam.w_u(d, th);
+      const double* wt = st ? fam.w_x(d, sth) : fam.w_u(d, sth);
       const double* h = st ? qd + s * nx : rd + s * nu;
       double dc = 0.0, cv = 0.0;
       for (int i = 0; i < n; ++i) {
-        const double dx = zq[off + i] - zo[off + i];
-        const double g = diag_cost_grad(fam.scale, w[i], zo[off + i]);
+        const double dx = szq[off + i] - szo[off + i];
+        const double g = diag_cost_grad(fam.scale, wt[i], szo[off + i]);
         const double qdx = h[i] * dx;
         dc = i == 0 ? g * dx : dc + g * dx;
         cv = i == 0 ? dx * qdx : cv + dx * qdx;
@@ -137,13 +163,14 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
     }
     for (int task = tid; task < nver * (2 * T + 2); task += blockDim.x) {
       const int ver = task / (2 * T + 2);
-      const int tt = task % (2 * T + 2);
-      merit_task(d, fam, th, zo, zq, ver == 0 ? 0.0 : cfg.alphas[ver - 1], ver > 0, tt,
-                 slots + static_cast<long>(ver) * nslot);
+      const int tt = task - ver * (2 * T + 2);
+      merit_task<NX, NU>(d, fam, sth, szo, szq, ver == 0 ? 0.0 : cfg.alphas[ver - 1], ver > 0, tt,
+                         slots + static_cast<long>(ver) * nslot, &s_bad[ver]);
     }
     __syncthreads();
     if (tid == 0) {
       double dc = 0.0, cv = 0.0;
+#pragma unroll 4
       for (int t = 0; t < 2 * T + 1; ++t) {
         dc = dc + dterm[t];
         cv = cv + cterm[t];
@@ -152,18 +179,18 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
       s_cv = cv;
     } else if (tid - 1 < nver) {
       const int ver = tid - 1;
-      double c = 0.0, vv = 0.0;
-      int bad = -1;
-      const bool ok = merit_fold(d, slots + static_cast<long>(ver) * nslot, &c, &vv, &bad);
-      s_cost[ver] = c;
-      s_viol[ver] = vv;
-      s_bad[ver] = ok ? -1 : bad;
+      if (s_bad[ver] == 0x7fffffff) {
+        double c = 0.0, vv = 0.0;
+        merit_fold(d, slots + static_cast<long>(ver) * nslot, &c, &vv);
+        s_cost[ver] = c;
+        s_viol[ver] = vv;
+      }
     }
     __syncthreads();
     if (tid == 0) {
       int err_ver = -1;
       for (int ver = 0; ver < nver; ++ver)
-        if (s_bad[ver] >= 0) {
+        if (s_bad[ver] != 0x7fffffff) {
           err_ver = ver;
           break;
         }
@@ -202,20 +229,23 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
     }
     __syncthreads();
     const double alpha = s_alpha;
-    if (alpha < 0.0) continue;  // merit evaluation failed
+    if (alpha < 0.0) {  // merit evaluation failed
+      __syncthreads();
+      continue;
+    }
     // z_new = z_old.interpolate(z_qp, alpha) and the step norm (trajectory.hpp:57-68)
     double stepmax = 0.0;
     for (int e = tid; e < d.nz; e += blockDim.x) {
-      const double zn = zo[e] + alpha * (zq[e] - zo[e]);
+      const double zn = szo[e] + alpha * (szq[e] - szo[e]);
       if (!isfinite(zn)) s_nonfinite = 1;
-      stepmax = fmax(stepmax, fabs(zn - zo[e]));
+      stepmax = fmax(stepmax, fabs(zn - szo[e]));
     }
     stepmax = warp_max(stepmax);
     if ((tid & 31) == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_step), __double_as_longlong(stepmax));
     __syncthreads();
     const bool diverged = s_nonfinite != 0;
     if (!diverged)
-      for (int e = tid; e < d.nz; e += blockDim.x) zo[e] = zo[e] + alpha * (zq[e] - zo[e]);
+      for (int e = tid; e < d.nz; e += blockDim.x) zo[e] = szo[e] + alpha * (szq[e] - szo[e]);
     if (tid == 0) {
       v.mu[p] = s_mu;
       v.alpha[p] = alpha;
@@ -233,32 +263,46 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
   }
 }
 
-/// ||kkt_residual(Z, LAMBDA)||_inf (problem.hpp:263-300), one CTA per problem.
-__global__ void kkt_kernel(View v, const int* __restrict__ work, const int* __restrict__ n_work) {
+/// ||kkt_residual(Z, LAMBDA)||_inf (problem.hpp:263-300), one CTA per
+/// problem with z, lambda and theta staged in shared memory, one thread per
+/// stage. NX, NU > 0 fix the block sizes at compile time.
+constexpr int kKktThreads = 128;
+template <int NX, int NU>
+__global__ void __launch_bounds__(kKktThreads) kkt_kernel(View v, const int* __restrict__ work,
+                                                        const int* __restrict__ n_work) {
+  extern __shared__ double sm_kkt[];
   __shared__ unsigned long long s_max;
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, T = d.T;
+  const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T;
+  constexpr int AX = NX ? NX : kMaxNx, AU = NU ? NU : kMaxNx;
   const Family fam = Family::from(v.prob);
+  double* z = sm_kkt;          // [nz]
+  double* lam = z + d.nz;      // [nl]
+  double* th = lam + d.nl;     // [nth]
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
     if (v.status[p].code != DOCP_OK) continue;
     if (threadIdx.x == 0) s_max = 0ull;
+    for (int e = threadIdx.x; e < d.nz; e += blockDim.x) z[e] = v.z[static_cast<long>(p) * d.nz + e];
+    for (int e = threadIdx.x; e < d.nl; e += blockDim.x) lam[e] = v.lam[static_cast<long>(p) * d.nl + e];
+    for (int e = threadIdx.x; e < d.nth; e += blockDim.x) th[e] = v.theta[static_cast<long>(p) * d.nth + e];
     __syncthreads();
-    const double* th = v.theta + static_cast<long>(p) * d.nth;
-    const double* z = v.z + static_cast<long>(p) * d.nz;
-    const double* lam = v.lam + static_cast<long>(p) * d.nl;
     double m = 0.0;
     for (int t = threadIdx.x; t <= T; t += blockDim.x) {
-      double jx[kMaxNx * kMaxNx], ju[kMaxNx * kMaxNx], res[kMaxNx];
+      double jx[AX * AX], ju[AX * AU], res[AX];
       const double* wx = fam.w_x(d, th);
       // grad_l for x_t: cost grad, + lambda_t (A+_{t-1}' lambda_t, or lambda_0 last), + A_t' lambda_{t+1}
-      if (t < T) fam.dynamics(d, th, z + xoff(d, t + 1), z + xoff(d, t), z + uoff(d, t), res, jx, ju);
-      for (int i = 0; i < nx; ++i) {
+      if (t < T) fam.dynamics<NX, NU>(d, th, z + xoff(d, t + 1), z + xoff(d, t), z + uoff(d, t), res, jx, ju);
+#pragma unroll
+      for (int i = 0; i < AX; ++i) {
+        if (i >= nx) break;
         double g = diag_cost_grad(fam.scale, wx[i], z[xoff(d, t) + i]);
         double a = 0.0;
         if (t < T) {
           a = jx[i * nx] * lam[(t + 1) * nx];
-          for (int k = 1; k < nx; ++k) a = a + jx[k + i * nx] * lam[(t + 1) * nx + k];
+#pragma unroll
+          for (int k = 1; k < AX; ++k)
+            if (k < nx) a = a + jx[k + i * nx] * lam[(t + 1) * nx + k];
         }
         if (t == 0) {
           if (t < T) g = g + a;
@@ -271,13 +315,19 @@ __global__ void kkt_kernel(View v, const int* __restrict__ work, const int* __re
       }
       if (t < T) {
         const double* wu = fam.w_u(d, th);
-        for (int i = 0; i < nu; ++i) {
+#pragma unroll
+        for (int i = 0; i < AU; ++i) {
+          if (i >= nu) break;
           double g = diag_cost_grad(fam.scale, wu[i], z[uoff(d, t) + i]);
           double a = ju[i * nx] * lam[(t + 1) * nx];
-          for (int k = 1; k < nx; ++k) a = a + ju[k + i * nx] * lam[(t + 1) * nx + k];
+#pragma unroll
+          for (int k = 1; k < AX; ++k)
+            if (k < nx) a = a + ju[k + i * nx] * lam[(t + 1) * nx + k];
           m = fmax(m, fabs(g + a));
         }
-        for (int i = 0; i < nx; ++i) m = fmax(m, fabs(res[i]));
+#pragma unroll
+        for (int i = 0; i < AX; ++i)
+          if (i < nx) m = fmax(m, fabs(res[i]));
       } else {
         const double* x_s = fam.x_s(d, th);
         for (int i = 0; i < nx; ++i) m = fmax(m, fabs(z[i] - x_s[i]));
