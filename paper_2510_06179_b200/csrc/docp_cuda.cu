@@ -119,7 +119,7 @@ __global__ void reset_status_kernel(View v) {
 template <int NX, int NU>
 int launch_assemble_t(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur) {
   constexpr int NG = kAsmGroupThreads / NX;
-  const size_t smem = static_cast<size_t>(NG) * (5 * NX * NX + 2 * NX * NU) * sizeof(double);
+  const size_t smem = static_cast<size_t>(NG) * AsmLayout<NX, NU>::GBUF * sizeof(double);
   auto kern = assemble_kernel_t<NX, NU>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;

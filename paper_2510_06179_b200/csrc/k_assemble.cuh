@@ -361,14 +361,31 @@ constexpr int kAsmGroupThreads = 128;
 /// (2 divisions per entry, as the reference's LLT solves), then chi_t, phi_t,
 /// chol(chi_t), chi_t^-1 and the stair off-diagonal follow with the same
 /// operation order as the runtime-shape kernel (bit-identical results).
+///
+/// Shared-memory layout: every group matrix is column-major with a padded
+/// leading dimension (NX + 1 rows, NU + 1 for M2), and group buffers are
+/// skewed by NX/2 doubles mod 16, so per-lane column walks, row walks and
+/// group-uniform (broadcast) reads all take the minimum number of wavefronts.
+template <int NX, int NU>
+struct AsmLayout {
+  static constexpr int LD = NX + 1;      // column stride of NX-row matrices
+  static constexpr int LDU = NU + 1;     // column stride of M2 (NU x NX)
+  static constexpr int P2 = NX * LD;     // padded NX x NX
+  static constexpr int PB = NU * LD;     // B_t, NX x NU
+  static constexpr int PM2 = NX * LDU;   // M2, NU x NX
+  static constexpr int RAW = 5 * P2 + PB + PM2;
+  static constexpr int SKEW = NX / 2;    // 16 bank pairs / (32 / NX) groups per warp
+  static constexpr int GBUF = RAW + ((SKEW - RAW % 16) % 16 + 16) % 16;
+};
+
 template <int NX, int NU>
 __global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v, const int* __restrict__ work,
                                                                       const int* __restrict__ n_work, double eps_pd,
                                                                       int do_schur) {
   static_assert(32 % NX == 0, "group size must divide the warp");
+  using Lay = AsmLayout<NX, NU>;
   constexpr int B2 = NX * NX;
-  constexpr int BU = NX * NU;
-  constexpr int GBUF = 5 * B2 + 2 * BU;  // doubles of scratch per group
+  constexpr int LD = Lay::LD, LDU = Lay::LDU;
   constexpr int NG = kAsmGroupThreads / NX;
   extern __shared__ double sm_asm[];
   __shared__ AsmShared sh;
@@ -377,24 +394,34 @@ __global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v,
   const int tid = threadIdx.x;
   const int g = tid / NX, l = tid % NX;
   const unsigned gmask = ((NX == 32 ? 0xffffffffu : ((1u << NX) - 1u))) << ((tid & 31) / NX * NX);
-  double* buf = sm_asm + static_cast<long>(g) * GBUF;
-  double* sA = buf;         // A_t            | P_t   (phase C)
-  double* sB = sA + B2;     // B_t
-  double* sM1 = sB + BU;    // M1 -> chol L   | sub_t (phase C)
-  double* sM2 = sM1 + B2;   // M2
-  double* sC = sM2 + BU;    // chi -> X=chi^-1| T1    (phase C)
-  double* sD = sC + B2;     // sym(chi)       | P_{t+1} (phase C)
-  double* sO = sD + B2;     // output block staged in the device layout
+  double* buf = sm_asm + static_cast<long>(g) * Lay::GBUF;
+  double* sA = buf;              // A_t            | P_t   (phase C)
+  double* sB = sA + Lay::P2;     // B_t
+  double* sM1 = sB + Lay::PB;    // M1 -> chol L   | sub_t (phase C)
+  double* sM2 = sM1 + Lay::P2;   // M2
+  double* sC = sM2 + Lay::PM2;   // chi -> X=chi^-1| T1    (phase C)
+  double* sD = sC + Lay::P2;     // sym(chi)       | P_{t+1} (phase C)
+  double* sO = sD + Lay::P2;     // output block staged in the device layout (padded columns)
+  // element (i, j) of an NX-row group matrix / of M2
+  auto ix = [](int i, int j) { return i + j * LD; };
+  auto iu = [](int i, int j) { return i + j * LDU; };
+  // staged output: device-layout offset o lives at (o / NX) * LD + o % NX
+  auto stage = [&](int b, int i, int j, double val) {
+    const int o = blk_off(NX, b, i, j);
+    sO[(o / NX) * LD + o % NX] = val;
+  };
   // coalesced copy of the staged block to block b of a region (16-byte stores)
   auto flush = [&](double* region, int b) {
     __syncwarp(gmask);
     double2* dst = reinterpret_cast<double2*>(region + static_cast<long>(b) * B2);
-    const double2* src = reinterpret_cast<const double2*>(sO);
 #pragma unroll
-    for (int k = l; k < B2 / 2; k += NX) dst[k] = src[k];
+    for (int k = l; k < B2 / 2; k += NX) {
+      const int o = 2 * k;  // NX even: o and o + 1 share a column
+      const double* src = sO + (o / NX) * LD + o % NX;
+      dst[k] = make_double2(src[0], src[1]);
+    }
     __syncwarp(gmask);
   };
-  auto stage = [&](int b, int i, int j, double val) { sO[blk_off(NX, b, i, j)] = val; };
 
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
@@ -416,38 +443,40 @@ __global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v,
       const double* lqt = lq + t * NX;
       const double* lqn = lq + (t + 1) * NX;
       const double* lrt = lr + t * NU;
+      const double* At = v.A + a_off(d, p, t);
+      const double* Bt = v.Bm + b_off(d, p, t);
 #pragma unroll
-      for (int k = l; k < B2; k += NX) sA[k] = v.A[a_off(d, p, t) + k];
+      for (int k = l; k < B2; k += NX) sA[ix(k % NX, k / NX)] = At[k];
 #pragma unroll
-      for (int k = l; k < BU; k += NX) sB[k] = v.Bm[b_off(d, p, t) + k];
+      for (int k = l; k < NX * NU; k += NX) sB[ix(k % NX, k / NX)] = Bt[k];
       __syncwarp(gmask);
       // M1(k, l) = (A(l,k)/lq_k)/lq_k ; M2(k, l) = (B(l,k)/lr_k)/lr_k
 #pragma unroll
-      for (int k = 0; k < NX; ++k) sM1[k + NX * l] = (sA[l + k * NX] / lqt[k]) / lqt[k];
+      for (int k = 0; k < NX; ++k) sM1[ix(k, l)] = (sA[ix(l, k)] / lqt[k]) / lqt[k];
 #pragma unroll
-      for (int k = 0; k < NU; ++k) sM2[k + NU * l] = (sB[l + k * NX] / lrt[k]) / lrt[k];
+      for (int k = 0; k < NU; ++k) sM2[iu(k, l)] = (sB[ix(l, k)] / lrt[k]) / lrt[k];
       __syncwarp(gmask);
       // column l of chi = A M1 + B M2 + A+ Q+^-1 A+'  and of phi_t = A Q_t^-1
       const double c3 = (1.0 / lqn[l]) / lqn[l];
       const double dq = (1.0 / lqt[l]) / lqt[l];
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
-        double a = sA[i] * sM1[NX * l];
+        double a = sA[ix(i, 0)] * sM1[ix(0, l)];
 #pragma unroll
-        for (int m = 1; m < NX; ++m) a = a + sA[i + m * NX] * sM1[m + NX * l];
-        double b = sB[i] * sM2[NU * l];
+        for (int m = 1; m < NX; ++m) a = a + sA[ix(i, m)] * sM1[ix(m, l)];
+        double b = sB[ix(i, 0)] * sM2[iu(0, l)];
 #pragma unroll
-        for (int m = 1; m < NU; ++m) b = b + sB[i + m * NX] * sM2[m + NU * l];
-        sC[i + NX * l] = (a + b) + (i == l ? c3 : 0.0);
-        stage(t, i, l, sA[i + l * NX] * dq);
+        for (int m = 1; m < NU; ++m) b = b + sB[ix(i, m)] * sM2[iu(m, l)];
+        sC[ix(i, l)] = (a + b) + (i == l ? c3 : 0.0);
+        stage(t, i, l, sA[ix(i, l)] * dq);
       }
       flush(Ss, t);
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
-        const double dv = 0.5 * (sC[i + NX * l] + sC[l + NX * i]);
-        sD[i + NX * l] = dv;
+        const double dv = 0.5 * (sC[ix(i, l)] + sC[ix(l, i)]);
+        sD[ix(i, l)] = dv;
         stage(t + 1, i, l, dv);
-        sM1[i + NX * l] = 0.0;  // becomes L
+        sM1[ix(i, l)] = 0.0;  // becomes L
       }
       flush(Sd, t + 1);
       // Cholesky of chi_t (eigen_lite LLT): lane l computes row l
@@ -457,25 +486,25 @@ __global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v,
       for (int k = 0; k < NX; ++k) {
         double s = 0.0;
         if (k > 0) {
-          s = sL[k] * sL[k];
+          s = sL[ix(k, 0)] * sL[ix(k, 0)];
 #pragma unroll
-          for (int j = 1; j < k; ++j) s = s + sL[k + j * NX] * sL[k + j * NX];
+          for (int j = 1; j < k; ++j) s = s + sL[ix(k, j)] * sL[ix(k, j)];
         }
-        const double piv = sD[k + k * NX] - s;
+        const double piv = sD[ix(k, k)] - s;
         if (piv <= 0.0) {
           failed = true;
           break;
         }
         const double lk = sqrt(piv);
-        if (l == k) sL[k + k * NX] = lk;
+        if (l == k) sL[ix(k, k)] = lk;
         if (l > k) {
           double tt = 0.0;
           if (k > 0) {
-            tt = sL[l] * sL[k];
+            tt = sL[ix(l, 0)] * sL[ix(k, 0)];
 #pragma unroll
-            for (int j = 1; j < k; ++j) tt = tt + sL[l + j * NX] * sL[k + j * NX];
+            for (int j = 1; j < k; ++j) tt = tt + sL[ix(l, j)] * sL[ix(k, j)];
           }
-          sL[l + k * NX] = (sD[l + k * NX] - tt) / lk;
+          sL[ix(l, k)] = (sD[ix(l, k)] - tt) / lk;
         }
         __syncwarp(gmask);
       }
@@ -492,29 +521,29 @@ __global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v,
         for (int i = 0; i < NX; ++i) {
           double s = 0.0;
           if (i > 0) {
-            s = sL[i] * x[0];
+            s = sL[ix(i, 0)] * x[0];
 #pragma unroll
-            for (int j = 1; j < i; ++j) s = s + sL[i + j * NX] * x[j];
+            for (int j = 1; j < i; ++j) s = s + sL[ix(i, j)] * x[j];
           }
-          x[i] = ((i == l ? 1.0 : 0.0) - s) / sL[i + i * NX];
+          x[i] = ((i == l ? 1.0 : 0.0) - s) / sL[ix(i, i)];
         }
 #pragma unroll
         for (int i = NX - 1; i >= 0; --i) {
           double s = 0.0;
           if (i + 1 < NX) {
-            s = sL[i + 1 + i * NX] * x[i + 1];
+            s = sL[ix(i + 1, i)] * x[i + 1];
 #pragma unroll
-            for (int j = i + 2; j < NX; ++j) s = s + sL[j + i * NX] * x[j];
+            for (int j = i + 2; j < NX; ++j) s = s + sL[ix(j, i)] * x[j];
           }
-          x[i] = (x[i] - s) / sL[i + i * NX];
+          x[i] = (x[i] - s) / sL[ix(i, i)];
         }
         __syncwarp(gmask);  // everyone is done reading chi (sC) before it becomes X
 #pragma unroll
-        for (int i = 0; i < NX; ++i) sX[i + NX * l] = x[i];
+        for (int i = 0; i < NX; ++i) sX[ix(i, l)] = x[i];
       }
       __syncwarp(gmask);
 #pragma unroll
-      for (int i = 0; i < NX; ++i) stage(t + 1, i, l, 0.5 * (sX[i + NX * l] + sX[l + NX * i]));
+      for (int i = 0; i < NX; ++i) stage(t + 1, i, l, 0.5 * (sX[ix(i, l)] + sX[ix(l, i)]));
       flush(Pd, t + 1);
     }
     __syncthreads();
@@ -528,25 +557,25 @@ __global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v,
     for (int t = g; t < T; t += NG) {
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
-        sA[i + NX * l] = blk_load(Pd, NX, t, i, l);
-        sM1[i + NX * l] = blk_load(Ss, NX, t, i, l);
-        sD[i + NX * l] = blk_load(Pd, NX, t + 1, i, l);
+        sA[ix(i, l)] = blk_load(Pd, NX, t, i, l);
+        sM1[ix(i, l)] = blk_load(Ss, NX, t, i, l);
+        sD[ix(i, l)] = blk_load(Pd, NX, t + 1, i, l);
       }
       __syncwarp(gmask);
       // T1(i, l) = sum_m (-P_t(i,m)) sub_t(l,m)
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
-        double a = (-sA[i]) * sM1[l];
+        double a = (-sA[ix(i, 0)]) * sM1[ix(l, 0)];
 #pragma unroll
-        for (int m = 1; m < NX; ++m) a = a + (-sA[i + m * NX]) * sM1[l + m * NX];
-        sC[i + NX * l] = a;
+        for (int m = 1; m < NX; ++m) a = a + (-sA[ix(i, m)]) * sM1[ix(l, m)];
+        sC[ix(i, l)] = a;
       }
       __syncwarp(gmask);
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
-        double a = sC[i] * sD[NX * l];
+        double a = sC[ix(i, 0)] * sD[ix(0, l)];
 #pragma unroll
-        for (int m = 1; m < NX; ++m) a = a + sC[i + m * NX] * sD[m + NX * l];
+        for (int m = 1; m < NX; ++m) a = a + sC[ix(i, m)] * sD[ix(m, l)];
         stage(t, i, l, a);
       }
       flush(Pu, t);
