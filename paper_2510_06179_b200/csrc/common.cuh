@@ -65,6 +65,24 @@ __host__ __device__ inline int blk_off(int nx, int b, int e, int s) {
   return s * nx + e;
 }
 
+/// Inverse of blk_off: the entry (e, s) stored at offset o of block b.
+__host__ __device__ inline void blk_entry(int nx, int b, int o, int* e, int* s) {
+  if (nx == 8) {
+    const int ss = (o >> 3) ^ (b & 1);
+    const int ch = ((o >> 1) & 3) ^ ((b >> 1) & 1) ^ (((ss >> 2) & 1) << 1);
+    *s = ss;
+    *e = (ch << 1) | (o & 1);
+    return;
+  }
+  if (nx == 4) {
+    *s = (o >> 2) ^ (b & 3);
+    *e = ((((o >> 1) & 1) ^ ((b >> 2) & 1)) << 1) | (o & 1);
+    return;
+  }
+  *s = o / nx;
+  *e = o % nx;
+}
+
 /// Iterate-vector layout in shared memory (block j, entry e): conflict-free
 /// LDS.128/STS.128 by 8 consecutive block rows.
 __host__ __device__ inline int vec_off(int nx, int j, int e) {

@@ -41,10 +41,12 @@ struct AsmShared {
 
 /// Phase A of K1 (problem.hpp:202-257): one thread per stage task. Writes the
 /// QpData of problem p and the first-error ranks; returns (block-uniform)
-/// whether the Schur phases may run. Ends with a __syncthreads.
+/// whether the Schur phases may run. Ends with a __syncthreads. NX, NU > 0
+/// fix the block sizes at compile time (same arithmetic).
+template <int NX = 0, int NU = 0>
 __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schur, AsmShared& sh) {
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, T = d.T, bsz = d.bsz;
+  const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T, bsz = nx * nx;
   const Family fam = Family::from(v.prob);
   const int tid = threadIdx.x;
   const double* th = v.theta + static_cast<long>(p) * d.nth;
@@ -71,7 +73,7 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
     if (task <= T) {  // state cost at x_t (problem.hpp:221-230)
       const int t = task;
       const double* x = z + xoff(d, t);
-      bool finite = isfinite(diag_cost_value(fam.scale, wx, x, nx));
+      bool finite = isfinite(diag_cost_value<NX>(fam.scale, wx, x, nx));
       bool pass = true, below = false;
       for (int i = 0; i < nx; ++i) {
         const double g = diag_cost_grad(fam.scale, wx[i], x[i]);
@@ -96,7 +98,7 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
       const double* x = z + xoff(d, t);
       const double* u = z + uoff(d, t);
       const double* xn = z + xoff(d, t + 1);
-      bool finite = isfinite(diag_cost_value(fam.scale, wu, u, nu));
+      bool finite = isfinite(diag_cost_value<NU>(fam.scale, wu, u, nu));
       bool pass = true, below = false;
       for (int i = 0; i < nu; ++i) {
         const double g = diag_cost_grad(fam.scale, wu[i], u[i]);
@@ -116,12 +118,12 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
         if (!(hr > 0.0) && !isnan(hr)) atomicMin(&sh.rank_qr, T + 1 + t);
         lr[t * nu + i] = sqrt(hr);
       }
-      double res[kMaxNx];
+      double res[NX ? NX : kMaxNx];
       // time-invariant families: one Jacobian copy, written by stage 0
       const bool write_jac = tv || t == 0;
       double* jx = v.A + a_off(d, p, t);
       double* ju = v.Bm + b_off(d, p, t);
-      fam.dynamics(d, th, xn, x, u, res, write_jac ? jx : nullptr, write_jac ? ju : nullptr);
+      fam.dynamics<NX, NU>(d, th, xn, x, u, res, write_jac ? jx : nullptr, write_jac ? ju : nullptr);
       bool dfin = true;
       for (int i = 0; i < nx; ++i) dfin = dfin && isfinite(res[i]);
       if (write_jac) {
@@ -362,10 +364,12 @@ constexpr int kAsmGroupThreads = 128;
 /// chol(chi_t), chi_t^-1 and the stair off-diagonal follow with the same
 /// operation order as the runtime-shape kernel (bit-identical results).
 ///
-/// Shared-memory layout: every group matrix is column-major with a padded
-/// leading dimension (NX + 1 rows, NU + 1 for M2), and group buffers are
-/// skewed by NX/2 doubles mod 16, so per-lane column walks, row walks and
-/// group-uniform (broadcast) reads all take the minimum number of wavefronts.
+/// Shared-memory layout: every group matrix (the staged output block too) is
+/// column-major with a padded leading dimension (NX + 1 rows, NU + 1 for M2),
+/// and consecutive group buffers are skewed by NX doubles mod 16. A 64-bit
+/// access is served per half-warp (16 lanes = 16 bank pairs), which holds
+/// 16 / NX groups; with this skew their per-lane column walks, row walks and
+/// group-uniform (broadcast) accesses hit distinct bank pairs.
 template <int NX, int NU>
 struct AsmLayout {
   static constexpr int LD = NX + 1;      // column stride of NX-row matrices
@@ -373,8 +377,10 @@ struct AsmLayout {
   static constexpr int P2 = NX * LD;     // padded NX x NX
   static constexpr int PB = NU * LD;     // B_t, NX x NU
   static constexpr int PM2 = NX * LDU;   // M2, NU x NX
-  static constexpr int RAW = 5 * P2 + PB + PM2;
-  static constexpr int SKEW = NX / 2;    // 16 bank pairs / (32 / NX) groups per warp
+  // B_t and M2 are dead once chi is formed; the staged output block reuses them
+  static constexpr int U = (PB + PM2) > P2 ? (PB + PM2) : P2;
+  static constexpr int RAW = 4 * P2 + U;
+  static constexpr int SKEW = NX % 16;   // groups of one half-warp on disjoint bank pairs
   static constexpr int GBUF = RAW + ((SKEW - RAW % 16) % 16 + 16) % 16;
 };
 
@@ -396,36 +402,33 @@ __global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v,
   const unsigned gmask = ((NX == 32 ? 0xffffffffu : ((1u << NX) - 1u))) << ((tid & 31) / NX * NX);
   double* buf = sm_asm + static_cast<long>(g) * Lay::GBUF;
   double* sA = buf;              // A_t            | P_t   (phase C)
-  double* sB = sA + Lay::P2;     // B_t
-  double* sM1 = sB + Lay::PB;    // M1 -> chol L   | sub_t (phase C)
-  double* sM2 = sM1 + Lay::P2;   // M2
-  double* sC = sM2 + Lay::PM2;   // chi -> X=chi^-1| T1    (phase C)
+  double* sM1 = sA + Lay::P2;    // M1 -> chol L   | sub_t (phase C)
+  double* sC = sM1 + Lay::P2;    // chi -> X=chi^-1| T1    (phase C)
   double* sD = sC + Lay::P2;     // sym(chi)       | P_{t+1} (phase C)
-  double* sO = sD + Lay::P2;     // output block staged in the device layout (padded columns)
+  double* sB = sD + Lay::P2;     // B_t            } until chi is formed
+  double* sM2 = sB + Lay::PB;    // M2             }
+  double* sO = sB;               // output block (logical (i, j) layout; flush permutes)
   // element (i, j) of an NX-row group matrix / of M2
   auto ix = [](int i, int j) { return i + j * LD; };
   auto iu = [](int i, int j) { return i + j * LDU; };
-  // staged output: device-layout offset o lives at (o / NX) * LD + o % NX
-  auto stage = [&](int b, int i, int j, double val) {
-    const int o = blk_off(NX, b, i, j);
-    sO[(o / NX) * LD + o % NX] = val;
-  };
-  // coalesced copy of the staged block to block b of a region (16-byte stores)
+  auto stage = [&](int /*b*/, int i, int j, double val) { sO[ix(i, j)] = val; };
+  // coalesced copy of the staged block to block b of a region in the device
+  // layout (16-byte stores; offsets o, o + 1 hold entries (e, s), (e + 1, s))
   auto flush = [&](double* region, int b) {
     __syncwarp(gmask);
     double2* dst = reinterpret_cast<double2*>(region + static_cast<long>(b) * B2);
 #pragma unroll
     for (int k = l; k < B2 / 2; k += NX) {
-      const int o = 2 * k;  // NX even: o and o + 1 share a column
-      const double* src = sO + (o / NX) * LD + o % NX;
-      dst[k] = make_double2(src[0], src[1]);
+      int e, sc;
+      blk_entry(NX, b, 2 * k, &e, &sc);
+      dst[k] = make_double2(sO[ix(e, sc)], sO[ix(e + 1, sc)]);
     }
     __syncwarp(gmask);
   };
 
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
-    if (!phase_linearize(v, p, eps_pd, do_schur, sh)) {
+    if (!phase_linearize<NX, NU>(v, p, eps_pd, do_schur, sh)) {
       __syncthreads();
       continue;
     }
@@ -468,8 +471,10 @@ __global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v,
 #pragma unroll
         for (int m = 1; m < NU; ++m) b = b + sB[ix(i, m)] * sM2[iu(m, l)];
         sC[ix(i, l)] = (a + b) + (i == l ? c3 : 0.0);
-        stage(t, i, l, sA[ix(i, l)] * dq);
       }
+      __syncwarp(gmask);  // B_t / M2 are dead: sO takes their place
+#pragma unroll
+      for (int i = 0; i < NX; ++i) stage(t, i, l, sA[ix(i, l)] * dq);
       flush(Ss, t);
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
