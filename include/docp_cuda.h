@@ -232,12 +232,16 @@ typedef struct docp_profile {
   uint64_t pcg_solves;                   /* PCG solves performed */
   double pcg_bytes_per_iteration;        /* B_it = 16 n_x^2 (2T+1) */
   double pcg_algorithmic_bytes;          /* (iterations + solves) B_it + solves 24 n_lambda */
+  double span_ms;                        /* first profiled launch start -> last profiled launch end */
+  double gap_ms;                         /* span minus the profiled launches (other ops, launch gaps) */
+  double max_gap_ms;                     /* largest single gap between consecutive profiled launches */
+  int32_t max_gap_after, max_gap_before; /* docp_prof_kind on either side of that gap */
 } docp_profile;
 int docp_profile_begin(docp_batch* batch);
 int docp_profile_end(docp_batch* batch, docp_profile* out);
 
 /* ---- diagnostics --------------------------------------------------------- */
-uint64_t docp_pcg_invocations(void);      /* PCG system solves performed (one per problem per solve) */
+uint64_t docp_pcg_invocations(void);      /* PCG system solves performed (one per problem per solve; counted on the device, synchronizes) */
 uint64_t docp_kernel_launches(void);      /* kernels this library has launched */
 const char* docp_last_error(void);        /* thread-local message of the last failing call */
 /* Reference-style message for a per-problem status (e.g. "pcg: p'Sp <= 0 ...

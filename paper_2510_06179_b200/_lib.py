@@ -51,7 +51,9 @@ PROF_NAMES = ("assemble", "gamma", "pcg", "recover", "step", "kkt", "vjp")
 class Profile(C.Structure):
     _fields_ = [("launches", C.c_int32 * PROF_KINDS), ("ms", C.c_double * PROF_KINDS),
                 ("pcg_iterations", C.c_uint64), ("pcg_solves", C.c_uint64),
-                ("pcg_bytes_per_iteration", C.c_double), ("pcg_algorithmic_bytes", C.c_double)]
+                ("pcg_bytes_per_iteration", C.c_double), ("pcg_algorithmic_bytes", C.c_double),
+                ("span_ms", C.c_double), ("gap_ms", C.c_double), ("max_gap_ms", C.c_double),
+                ("max_gap_after", C.c_int32), ("max_gap_before", C.c_int32)]
 
 
 # every symbol include/docp_cuda.h declares, with its ctypes signature

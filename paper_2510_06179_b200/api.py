@@ -305,7 +305,10 @@ class Batch:
         kinds = {n: {"launches": int(p.launches[i]), "ms": float(p.ms[i])} for i, n in enumerate(L.PROF_NAMES)}
         return {"kernels": kinds, "pcg_iterations": int(p.pcg_iterations), "pcg_solves": int(p.pcg_solves),
                 "pcg_bytes_per_iteration": float(p.pcg_bytes_per_iteration),
-                "pcg_algorithmic_bytes": float(p.pcg_algorithmic_bytes)}
+                "pcg_algorithmic_bytes": float(p.pcg_algorithmic_bytes),
+                "span_ms": float(p.span_ms), "gap_ms": float(p.gap_ms), "max_gap_ms": float(p.max_gap_ms),
+                "max_gap_between": [L.PROF_NAMES[k] if 0 <= k < len(L.PROF_NAMES) else None
+                                    for k in (p.max_gap_after, p.max_gap_before)]}
 
     # ---- primitives (one call each for the whole batch)
     def linearize(self, eps_pd: float = 1e-6):

@@ -16,7 +16,6 @@
 
 namespace docp_host {
 
-extern std::atomic<uint64_t> g_pcg_invocations;
 extern std::atomic<uint64_t> g_launches;
 int fail(int code, const char* fmt, ...);
 
@@ -54,6 +53,11 @@ struct docp_batch {
   // profiling: CUDA events around every launch, per kernel kind, on the batch stream
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[DOCP_PROF_KINDS];
+  struct ProfRec {
+    int kind;
+    cudaEvent_t start, stop;
+  };
+  std::vector<ProfRec> prof_seq;  // every profiled launch in stream order
   std::vector<cudaEvent_t> event_pool;
   size_t pool_used = 0;
 
@@ -91,6 +95,7 @@ struct ProfScope {
     stop = pool_event(b);
     cudaEventRecord(start, b->stream);
     b->prof[kind].emplace_back(start, stop);
+    b->prof_seq.push_back({kind, start, stop});
   }
   ~ProfScope() {
     if (stop) cudaEventRecord(stop, b->stream);

@@ -130,7 +130,7 @@ struct View {
   docp_status* status;
   int *sqp_iters, *converged, *pcg_iters, *pcg_conv, *pcg_hist, *pd_proj, *accepted;
   double *kkt, *final_eta, *step_sizes, *mu, *alpha, *loss;
-  unsigned long long* pcg_acc;  // [0] iterations, [1] solves (roofline accounting)
+  unsigned long long* pcg_acc;  // [0] iterations, [1] solves (roofline accounting), [2] lifetime solves
   int max_hist;
 };
 

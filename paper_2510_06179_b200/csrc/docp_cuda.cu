@@ -13,6 +13,9 @@
 #include <string>
 #include <vector>
 
+#include <mutex>
+#include <set>
+
 #include "batch.cuh"
 #include "families.cuh"
 #include "k_assemble.cuh"
@@ -24,8 +27,20 @@ using namespace docp_host;
 namespace docp_host {
 
 thread_local std::string g_last_error;
-std::atomic<uint64_t> g_pcg_invocations{0};
 std::atomic<uint64_t> g_launches{0};
+// PCG solves are counted on the device (one per problem the kernel actually
+// solves, pcg.hpp:57); docp_pcg_invocations sums the live batches' counters
+// and those of destroyed batches.
+std::mutex g_batches_mu;
+std::set<docp_batch*> g_batches;
+uint64_t g_retired_solves = 0;
+
+uint64_t batch_solves(docp_batch* b) {
+  unsigned long long n = 0;
+  if (cudaStreamSynchronize(b->stream) != cudaSuccess) return 0;
+  if (cudaMemcpy(&n, b->v.pcg_acc + 2, sizeof n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return n;
+}
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -190,7 +205,6 @@ int launch_pcg(docp_batch* b, const docp_pcg_config& cfg, const int* list, const
   if (!(cfg.epsilon > 0.0 && cfg.max_iters >= 0)) return fail(DOCP_DIMENSION, "pcg: invalid config");
   const bool par = cfg.mode == DOCP_PCG_PARITY;
   const PcgPlan pl = plan_pcg(b);
-  g_pcg_invocations.fetch_add(static_cast<uint64_t>(n_hint), std::memory_order_relaxed);
   switch (b->d.nx) {
     case 4: return launch_pcg_nx4(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
     case 8: return launch_pcg_nx8(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
@@ -388,7 +402,7 @@ int docp_batch_create(const docp_problem* problem, int32_t batch_size, int32_t d
   A(b->list[0], B);
   A(b->list[1], B);
   A(b->counts, 8);
-  A(v.pcg_acc, 2);
+  A(v.pcg_acc, 3);
 #undef A
   if ((rc = ensure_hist(b, 20))) {
     delete b;
@@ -404,11 +418,22 @@ int docp_batch_create(const docp_problem* problem, int32_t batch_size, int32_t d
     delete b;
     return fail(DOCP_CUDA_ERROR, "batch init failed");
   }
+  {
+    std::lock_guard<std::mutex> lk(g_batches_mu);
+    g_batches.insert(b);
+  }
   *out = b;
   return DOCP_OK;
 }
 
-void docp_batch_destroy(docp_batch* b) { delete b; }
+void docp_batch_destroy(docp_batch* b) {
+  if (!b) return;
+  {
+    std::lock_guard<std::mutex> lk(g_batches_mu);
+    if (g_batches.erase(b)) g_retired_solves += batch_solves(b);
+  }
+  delete b;
+}
 
 int docp_batch_set_stream(docp_batch* b, void* stream) {
   if (!b) return fail(DOCP_INVALID, "null batch");
@@ -603,23 +628,29 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
   CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, 2 * sizeof(int), b->stream));
   init_solve_kernel<<<grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8), 256, 0, b->stream>>>(b->v, b->list[0], b->counts + 1);
   LAUNCH_CHECK();
-  int n_active = 0;
-  if ((rc = read_count(b, b->counts + 1, &n_active))) return rc;
-  for (int iter = 0; iter < cfg->max_sqp_iters && n_active > 0; ++iter) {
+  // The loop is enqueued without waiting on the device: every kernel reads
+  // the active count from device memory and exits early when it is zero, so
+  // iterations after global convergence cost a few empty launches. The host
+  // reads the count back only at iterations 4, 8, 16, ... to stop early
+  // (one synchronisation for the benchmark's max_sqp_iters = 5).
+  int n_bound = b->B;  // upper bound of the active count, sizes the grids
+  for (int iter = 0; iter < cfg->max_sqp_iters && n_bound > 0; ++iter) {
     const int* list = b->list[cur];
     const int* cnt = b->counts + 1 + cur;
-    if ((rc = launch_assemble(b, list, cnt, n_active, cfg->eps_pd, 1))) return rc;
-    if ((rc = launch_gamma(b, list, cnt, n_active, DOCP_RHS_FORWARD))) return rc;
-    if ((rc = launch_pcg(b, cfg->pcg, list, cnt, n_active, b->v.lam))) return rc;
-    if ((rc = launch_recover(b, list, cnt, n_active, b->v.lam, DOCP_RHS_FORWARD))) return rc;
-    if ((rc = launch_step(b, *cfg, list, cnt, n_active, iter, 1))) return rc;
+    if ((rc = launch_assemble(b, list, cnt, n_bound, cfg->eps_pd, 1))) return rc;
+    if ((rc = launch_gamma(b, list, cnt, n_bound, DOCP_RHS_FORWARD))) return rc;
+    if ((rc = launch_pcg(b, cfg->pcg, list, cnt, n_bound, b->v.lam))) return rc;
+    if ((rc = launch_recover(b, list, cnt, n_bound, b->v.lam, DOCP_RHS_FORWARD))) return rc;
+    if ((rc = launch_step(b, *cfg, list, cnt, n_bound, iter, 1))) return rc;
     const int nxt = cur ^ 1;
     CUDA_TRY(cudaMemsetAsync(b->counts + 1 + nxt, 0, sizeof(int), b->stream));
-    compact_kernel<<<grid_for(n_active, 256, 4096), 256, 0, b->stream>>>(b->v, list, cnt, b->list[nxt],
-                                                                          b->counts + 1 + nxt);
+    compact_kernel<<<grid_for(n_bound, 256, 4096), 256, 0, b->stream>>>(b->v, list, cnt, b->list[nxt],
+                                                                         b->counts + 1 + nxt);
     LAUNCH_CHECK();
     cur = nxt;
-    if ((rc = read_count(b, b->counts + 1 + cur, &n_active))) return rc;
+    const int done = iter + 1;
+    if (done < cfg->max_sqp_iters && done >= 4 && (done & (done - 1)) == 0)
+      if ((rc = read_count(b, b->counts + 1 + cur, &n_bound))) return rc;
   }
   // refresh QP / Schur at the returned trajectory, KKT diagnostic (sqp.hpp:254-259)
   CUDA_TRY(cudaMemsetAsync(b->counts + 1 + (cur ^ 1), 0, sizeof(int), b->stream));
@@ -679,6 +710,7 @@ int docp_profile_begin(docp_batch* b) {
   if (!b) return fail(DOCP_INVALID, "null batch");
   CUDA_TRY(cudaStreamSynchronize(b->stream));
   for (auto& v : b->prof) v.clear();
+  b->prof_seq.clear();
   b->pool_used = 0;
   CUDA_TRY(cudaMemsetAsync(b->v.pcg_acc, 0, 2 * sizeof(unsigned long long), b->stream));
   b->profiling = true;
@@ -700,6 +732,22 @@ int docp_profile_end(docp_batch* b, docp_profile* out) {
     }
     out->ms[k] = ms;
   }
+  if (!b->prof_seq.empty()) {
+    float span = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&span, b->prof_seq.front().start, b->prof_seq.back().stop));
+    out->span_ms = span;
+    out->max_gap_after = out->max_gap_before = -1;
+    for (size_t k = 1; k < b->prof_seq.size(); ++k) {
+      float g = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&g, b->prof_seq[k - 1].stop, b->prof_seq[k].start));
+      out->gap_ms += g;
+      if (g > out->max_gap_ms) {
+        out->max_gap_ms = g;
+        out->max_gap_after = b->prof_seq[k - 1].kind;
+        out->max_gap_before = b->prof_seq[k].kind;
+      }
+    }
+  }
   unsigned long long acc[2];
   CUDA_TRY(cudaMemcpy(acc, b->v.pcg_acc, sizeof acc, cudaMemcpyDeviceToHost));
   out->pcg_iterations = acc[0];
@@ -712,7 +760,12 @@ int docp_profile_end(docp_batch* b, docp_profile* out) {
   return DOCP_OK;
 }
 
-uint64_t docp_pcg_invocations(void) { return g_pcg_invocations.load(); }
+uint64_t docp_pcg_invocations(void) {
+  std::lock_guard<std::mutex> lk(g_batches_mu);
+  uint64_t n = g_retired_solves;
+  for (docp_batch* b : g_batches) n += batch_solves(b);
+  return n;
+}
 uint64_t docp_kernel_launches(void) { return g_launches.load(); }
 const char* docp_last_error(void) { return g_last_error.c_str(); }
 

@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads) pcg_kernel(View v, const int* 
       else set_status(v.status + p, DOCP_BREAKDOWN, status, iters);
       atomicAdd(v.pcg_acc, static_cast<unsigned long long>(iters));
       atomicAdd(v.pcg_acc + 1, 1ull);
+      atomicAdd(v.pcg_acc + 2, 1ull);  // lifetime solves (docp_pcg_invocations)
     }
     __syncthreads();
   }

@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(MAXT) pcg_kernel_h8(View v, const int* __restr
       else set_status(v.status + p, DOCP_BREAKDOWN, status, iters);
       atomicAdd(v.pcg_acc, static_cast<unsigned long long>(iters));
       atomicAdd(v.pcg_acc + 1, 1ull);
+      atomicAdd(v.pcg_acc + 2, 1ull);  // lifetime solves (docp_pcg_invocations)
     }
     __syncthreads();
   }
