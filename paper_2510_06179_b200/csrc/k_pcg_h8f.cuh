@@ -1,0 +1,341 @@
+// k_pcg_h8f.cuh — K2 FAST mode for n_x = 8 with resident blocks: the
+// instruction-lean form of pcg_kernel_h8 (same algorithm, pcg.hpp:52-109,
+// same exit test / eta clamp / breakdown checks; FAST arithmetic).
+//
+// What changes against pcg_kernel_h8<FAST>:
+//  * block addressing is hoisted: for thread (i, h) the chunk holding rows
+//    4h + 2j, 4h + 2j + 1 of logical column c of a block lies at
+//        block + 8c + r(c) + 2 (j ^ m),   r(c) = +-8p + 4(h or 1-h)
+//    (p = i & 1, m = (i >> 1) & 1; common.cuh blk_off), so eight per-thread
+//    offsets and compile-time immediates replace the per-load swizzle math
+//    (the j ^ m term is what keeps a quarter-warp's four blocks on distinct
+//    banks, so it stays in the per-thread offsets);
+//  * no branches on the row: the CTA's block rows are padded to the thread
+//    count (vector buffers sized to match), rows past the last one compute
+//    on whatever their addresses hold and are masked out of every result
+//    (selects, not multiplies, so garbage NaNs cannot leak);
+//  * every 8-term accumulation runs as two 4-term partial sums (ILP).
+// Vector rows keep the conflict-free vec_off layout, with per-thread offsets.
+#pragma once
+
+#include "k_pcg.cuh"
+
+namespace docp_dev {
+
+namespace h8f {
+
+__device__ __forceinline__ double sel(bool c, double a, double b) { return c ? a : b; }
+
+/// Per-thread chunk offsets (in doubles, relative to a block): [k][j] for
+/// the column class k = (c >= 4) * 2 + (c & 1) and row pair j.
+struct Bases {
+  int o[4][2];
+};
+
+/// Rows 4h..4h+3 of all 8 columns of the block at `blk`: d[c][j] = rows
+/// 4h + 2j, 4h + 2j + 1 of column c.
+__device__ __forceinline__ void load_rows(const double* blk, const Bases& bs, double2 (&d)[8][2]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int k = (c >= 4) * 2 + (c & 1);
+    d[c][0] = *reinterpret_cast<const double2*>(blk + bs.o[k][0] + 8 * c);
+    d[c][1] = *reinterpret_cast<const double2*>(blk + bs.o[k][1] + 8 * c);
+  }
+}
+
+}  // namespace h8f
+
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __restrict__ work,
+                                                     const int* __restrict__ n_work, int* __restrict__ counter,
+                                                     double* __restrict__ sol_all, double epsilon,
+                                                     int max_iters_cfg) {
+  extern __shared__ __align__(128) double sm_pcg[];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ int s_work;
+  const Dims d = v.d;
+  const int nl = d.nl, nb = d.nb;
+  const int tid = threadIdx.x;
+  const int i = tid >> 1, h = tid & 1;
+  const bool act = i < nb;
+  const bool has_next = i + 1 < nb;
+  const bool has_prev = i > 0;
+  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int rows = blockDim.x >> 1;  // padded block rows
+
+  double* sblk = sm_pcg;
+  double* vbuf = sblk + d.blk_stride;  // [rows][8]
+  double* xbuf = vbuf + rows * 8;      // [rows][8]
+  double* red = xbuf + rows * 8;       // [64]
+
+  const int p = i & 1, m = (i >> 1) & 1;
+  h8f::Bases bs;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      bs.o[k][j] = ((k & 1) ? -8 * p : 8 * p) + 4 * ((k >> 1) ? 1 - h : h) + 2 * (j ^ m);
+
+  if (tid == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  const int max_iters = max_iters_cfg > 0 ? max_iters_cfg : 2 * nl;
+  const double threshold = epsilon * epsilon;
+
+  auto dot = [&](const double* a, const double* b) -> double {
+    double s = fma(a[3], b[3], fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0])));
+    s = act ? s : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    double t = red[0];
+    for (int k = 1; k < nw; ++k) t = t + red[k];
+    return t;
+  };
+  auto norm = [&](const double* a) -> double {
+    __syncthreads();
+    double s = fma(a[3], a[3], fma(a[2], a[2], fma(a[1], a[1], a[0] * a[0])));
+    s = act ? s : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) red[32 + warp] = s;
+    __syncthreads();
+    double t = red[32];
+    for (int k = 1; k < nw; ++k) t = t + red[32 + k];
+    return sqrt(t);
+  };
+
+  for (;;) {
+    if (tid == 0) s_work = atomicAdd(counter, 1);
+    __syncthreads();
+    const int w = s_work;
+    if (w >= *n_work) break;
+    const int pidx = work[w];
+    if (v.status[pidx].code != DOCP_OK) {
+      __syncthreads();
+      continue;
+    }
+    const double* rec = v.blocks + static_cast<long>(pidx) * d.blk_stride;
+    if (tid == 0) {
+      fence_proxy_async();
+      const uint32_t bytes = static_cast<uint32_t>((d.p_sup + ((static_cast<long>(d.T) * d.bsz + 1) & ~1L)) * 8);
+      mbar_arrive_expect_tx(&s_bar, bytes);
+      tma_bulk_g2s(sblk, rec, bytes, &s_bar);
+    }
+    const double* gam = v.gamma + static_cast<long>(pidx) * nl;
+    double* sol = sol_all + static_cast<long>(pidx) * nl;
+    // this thread's blocks (rows past the last one reuse its blocks; masked below)
+    const int ib = act ? i : nb - 1;
+    const int io = has_next ? i : 0;
+    const double* SdI = sblk + d.s_diag + ib * 64;
+    const double* PdI = sblk + d.p_diag + ib * 64;
+    const double* SsI = sblk + d.s_sub + io * 64;
+    const double* PuI = sblk + d.p_sup + io * 64;
+    // vector rows in the vec_off layout (common.cuh): chunk k of row j sits at
+    // j * 8 + 2 (k ^ ((j >> 1) & 3)); per-thread offsets of the chunks used
+    auto voff = [](int j, int k) { return j * 8 + 2 * (k ^ ((j >> 1) & 3)); };
+    const int my0 = voff(i, 2 * h), my1 = voff(i, 2 * h + 1);              // my half of row i
+    const int nx0 = voff(i + 1, 2 * h), nx1 = voff(i + 1, 2 * h + 1);      // ... of row i + 1
+    const int pv0 = voff(i - 1, 2 * h), pv1 = voff(i - 1, 2 * h + 1);      // ... of row i - 1
+    const int nf0 = voff(i + 1, 0), nf1 = voff(i + 1, 1), nf2 = voff(i + 1, 2), nf3 = voff(i + 1, 3);
+
+    double lam[4] = {0, 0, 0, 0}, r[4], pv[4], y[4];
+    if (act) {
+      const double2 a = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h);
+      const double2 b = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h + 2);
+      lam[0] = a.x, lam[1] = a.y, lam[2] = b.x, lam[3] = b.y;
+    }
+    mbar_wait(&s_bar, phase);
+    phase ^= 1;
+    __syncthreads();
+
+    // out = A x, A = -S (D = S_ii, O = L_i = S_{i+1,i}) or Phi^-1 (D = P_ii, O = U_i = P_{i,i+1}).
+    auto matvec = [&](bool precond, const double* xr, double* out) {
+      double other[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) other[q] = __shfl_xor_sync(0xffffffffu, xr[q], 1);
+      double xf[8];  // x_i in logical order
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        xf[q] = h8f::sel(h, other[q], xr[q]);
+        xf[4 + q] = h8f::sel(h, xr[q], other[q]);
+      }
+      *reinterpret_cast<double2*>(vbuf + my0) = make_double2(xr[0], xr[1]);
+      *reinterpret_cast<double2*>(vbuf + my1) = make_double2(xr[2], xr[3]);
+
+      // own = D x_i, two 4-column partial sums per row
+      double2 dd[8][2];
+      h8f::load_rows(precond ? PdI : SdI, bs, dd);
+      double oa[4], ob[4];
+      oa[0] = dd[0][0].x * xf[0], oa[1] = dd[0][0].y * xf[0], oa[2] = dd[0][1].x * xf[0], oa[3] = dd[0][1].y * xf[0];
+      ob[0] = dd[4][0].x * xf[4], ob[1] = dd[4][0].y * xf[4], ob[2] = dd[4][1].x * xf[4], ob[3] = dd[4][1].y * xf[4];
+#pragma unroll
+      for (int c = 1; c < 4; ++c) {
+        oa[0] = fma(dd[c][0].x, xf[c], oa[0]);
+        oa[1] = fma(dd[c][0].y, xf[c], oa[1]);
+        oa[2] = fma(dd[c][1].x, xf[c], oa[2]);
+        oa[3] = fma(dd[c][1].y, xf[c], oa[3]);
+        ob[0] = fma(dd[4 + c][0].x, xf[4 + c], ob[0]);
+        ob[1] = fma(dd[4 + c][0].y, xf[4 + c], ob[1]);
+        ob[2] = fma(dd[4 + c][1].x, xf[4 + c], ob[2]);
+        ob[3] = fma(dd[4 + c][1].y, xf[4 + c], ob[3]);
+      }
+      double own[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) own[q] = oa[q] + ob[q];
+
+      asm volatile("" ::: "memory");  // D is consumed: bound the live registers before O
+      double2 oo[8][2];
+      h8f::load_rows(precond ? PuI : SsI, bs, oo);
+      double hand[4];  // logical order, for block row i+1
+      if (precond) {   // U_i' x_i: half-column partial sums over my rows, partner completes
+        double part[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          part[c] = fma(oo[c][1].y, xr[3], fma(oo[c][1].x, xr[2], fma(oo[c][0].y, xr[1], oo[c][0].x * xr[0])));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double send = h8f::sel(h, part[q], part[4 + q]);
+          const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+          hand[q] = h8f::sel(h, part[4 + q], part[q]) + recv;
+        }
+      } else {  // L_i x_i, my rows
+        double ha[4], hb[4];
+        ha[0] = oo[0][0].x * xf[0], ha[1] = oo[0][0].y * xf[0], ha[2] = oo[0][1].x * xf[0], ha[3] = oo[0][1].y * xf[0];
+        hb[0] = oo[4][0].x * xf[4], hb[1] = oo[4][0].y * xf[4], hb[2] = oo[4][1].x * xf[4], hb[3] = oo[4][1].y * xf[4];
+#pragma unroll
+        for (int c = 1; c < 4; ++c) {
+          ha[0] = fma(oo[c][0].x, xf[c], ha[0]);
+          ha[1] = fma(oo[c][0].y, xf[c], ha[1]);
+          ha[2] = fma(oo[c][1].x, xf[c], ha[2]);
+          ha[3] = fma(oo[c][1].y, xf[c], ha[3]);
+          hb[0] = fma(oo[4 + c][0].x, xf[4 + c], hb[0]);
+          hb[1] = fma(oo[4 + c][0].y, xf[4 + c], hb[1]);
+          hb[2] = fma(oo[4 + c][1].x, xf[4 + c], hb[2]);
+          hb[3] = fma(oo[4 + c][1].y, xf[4 + c], hb[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) hand[q] = ha[q] + hb[q];
+      }
+      *reinterpret_cast<double2*>(xbuf + my0) = make_double2(hand[0], hand[1]);
+      *reinterpret_cast<double2*>(xbuf + my1) = make_double2(hand[2], hand[3]);
+      __syncthreads();
+
+      double up[4];  // logical order
+      if (!precond) {  // L_i' x_{i+1}: partial sums over my rows of x_{i+1}, partner completes
+        const double2 n0 = *reinterpret_cast<const double2*>(vbuf + nx0);
+        const double2 n1 = *reinterpret_cast<const double2*>(vbuf + nx1);
+        const double xn[4] = {n0.x, n0.y, n1.x, n1.y};
+        double part[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          part[c] = fma(oo[c][1].y, xn[3], fma(oo[c][1].x, xn[2], fma(oo[c][0].y, xn[1], oo[c][0].x * xn[0])));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double send = h8f::sel(h, part[q], part[4 + q]);
+          const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+          up[q] = h8f::sel(h, part[4 + q], part[q]) + recv;
+        }
+      } else {  // U_i x_{i+1}, my rows
+        const double2 t0 = *reinterpret_cast<const double2*>(vbuf + nf0);
+        const double2 t1 = *reinterpret_cast<const double2*>(vbuf + nf1);
+        const double2 t2 = *reinterpret_cast<const double2*>(vbuf + nf2);
+        const double2 t3 = *reinterpret_cast<const double2*>(vbuf + nf3);
+        const double xn[8] = {t0.x, t0.y, t1.x, t1.y, t2.x, t2.y, t3.x, t3.y};
+        double ua[4], ub[4];
+        ua[0] = oo[0][0].x * xn[0], ua[1] = oo[0][0].y * xn[0], ua[2] = oo[0][1].x * xn[0], ua[3] = oo[0][1].y * xn[0];
+        ub[0] = oo[4][0].x * xn[4], ub[1] = oo[4][0].y * xn[4], ub[2] = oo[4][1].x * xn[4], ub[3] = oo[4][1].y * xn[4];
+#pragma unroll
+        for (int c = 1; c < 4; ++c) {
+          ua[0] = fma(oo[c][0].x, xn[c], ua[0]);
+          ua[1] = fma(oo[c][0].y, xn[c], ua[1]);
+          ua[2] = fma(oo[c][1].x, xn[c], ua[2]);
+          ua[3] = fma(oo[c][1].y, xn[c], ua[3]);
+          ub[0] = fma(oo[4 + c][0].x, xn[4 + c], ub[0]);
+          ub[1] = fma(oo[4 + c][0].y, xn[4 + c], ub[1]);
+          ub[2] = fma(oo[4 + c][1].x, xn[4 + c], ub[2]);
+          ub[3] = fma(oo[4 + c][1].y, xn[4 + c], ub[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) up[q] = ua[q] + ub[q];
+      }
+      const double2 l0 = *reinterpret_cast<const double2*>(xbuf + pv0);
+      const double2 l1 = *reinterpret_cast<const double2*>(xbuf + pv1);
+      const double low[4] = {l0.x, l0.y, l1.x, l1.y};
+      // rows: diag, then sub (i > 0), then super (i < nb - 1)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double acc = own[q];
+        acc = has_prev ? acc + low[q] : acc;
+        acc = has_next ? acc + up[q] : acc;
+        out[q] = acc;
+      }
+    };
+
+    matvec(false, lam, y);  // y = (-S) lambda0
+    if (act) {
+      const double2 a = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h);
+      const double2 b = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h + 2);
+      r[0] = a.x - y[0], r[1] = a.y - y[1], r[2] = b.x - y[2], r[3] = b.y - y[3];
+    } else {
+      r[0] = r[1] = r[2] = r[3] = 0.0;
+    }
+    __syncthreads();  // every phase-2 read of lambda / its hand-over is done
+    matvec(true, r, pv);  // r~
+    double eta = dot(r, pv);
+    int status = DOCP_OK, iters = 0;
+    if (eta < 0.0) {
+      const double scale = norm(r) * norm(pv);
+      if (-eta <= 1e-10 * scale + 1e-300) eta = 0.0;
+      else status = DOCP_AT_PCG_PRECOND;
+    }
+
+    while (status == DOCP_OK && eta > threshold && iters < max_iters) {
+      matvec(false, pv, y);
+      const double vv = dot(pv, y);
+      if (vv <= 0.0) {
+        status = DOCP_AT_PCG_CURVATURE;
+        break;
+      }
+      const double alpha = eta / vv;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        lam[q] = fma(alpha, pv[q], lam[q]);
+        r[q] = fma(-alpha, y[q], r[q]);
+      }
+      matvec(true, r, y);  // r~ (y reused)
+      double eta_next = dot(r, y);
+      if (eta_next < 0.0) {
+        const double scale = norm(r) * norm(y);
+        if (-eta_next <= 1e-10 * scale + 1e-300) {
+          eta_next = 0.0;
+        } else {
+          status = DOCP_AT_PCG_PRECOND;
+          break;
+        }
+      }
+      const double beta = eta_next / eta;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pv[q] = fma(beta, pv[q], y[q]);
+      eta = eta_next;
+      ++iters;
+    }
+
+    if (act) {
+      *reinterpret_cast<double2*>(sol + i * 8 + 4 * h) = make_double2(lam[0], lam[1]);
+      *reinterpret_cast<double2*>(sol + i * 8 + 4 * h + 2) = make_double2(lam[2], lam[3]);
+    }
+    if (tid == 0) {
+      v.pcg_iters[pidx] = iters;
+      v.final_eta[pidx] = eta;
+      v.pcg_conv[pidx] = status == DOCP_OK && eta <= threshold;
+      if (status == DOCP_OK) set_status(v.status + pidx, DOCP_OK, DOCP_AT_NONE, 0);
+      else set_status(v.status + pidx, DOCP_BREAKDOWN, status, iters);
+      atomicAdd(v.pcg_acc, static_cast<unsigned long long>(iters));
+      atomicAdd(v.pcg_acc + 1, 1ull);
+      atomicAdd(v.pcg_acc + 2, 1ull);  // lifetime solves (docp_pcg_invocations)
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace docp_dev

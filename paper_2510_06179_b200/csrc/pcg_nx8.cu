@@ -1,5 +1,9 @@
 // pcg_nx8.cu — K2 instantiations for n_x = 8 (separate translation unit for build parallelism)
+#include <cstdlib>
+#include <cstring>
+
 #include "k_pcg_h8.cuh"
+#include "k_pcg_h8f.cuh"
 #include "pcg_launch.cuh"
 
 namespace docp_host {
@@ -22,9 +26,37 @@ int launch_h8(docp_batch* b, const PcgPlan& pl, const int* list, const int* coun
   return DOCP_OK;
 }
 
-/// n_x = 8: two threads per block row (pcg_kernel_h8) up to T = 255, one
-/// thread per block row (pcg_kernel) beyond.
+/// FAST with resident blocks: the instruction-lean pcg_kernel_h8f.
+int launch_h8f(docp_batch* b, const PcgPlan& pl, const int* list, const int* count, int n_hint, double* sol,
+               double eps, int max_iters) {
+  auto kern = pcg_kernel_h8f<256>;
+  const int threads = (2 * b->d.nb + 31) / 32 * 32;
+  const size_t smem = (static_cast<size_t>(b->d.blk_stride) + 2 * (threads / 2) * 8 + 64) * sizeof(double);
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit on an SM (smem %zu)", smem);
+  const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
+  CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
+  ProfScope ps(b, DOCP_PROF_PCG);
+  kern<<<grid, threads, smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+/// Kernel variant override for A/B measurements: DOCP_PCG_VARIANT=h8 keeps
+/// FAST solves on pcg_kernel_h8.
+static bool force_h8() {
+  const char* e = std::getenv("DOCP_PCG_VARIANT");
+  return e && std::strcmp(e, "h8") == 0;
+}
+
+/// n_x = 8: FAST + resident blocks -> pcg_kernel_h8f; otherwise two threads
+/// per block row (pcg_kernel_h8) up to T = 255, one thread per block row
+/// (pcg_kernel) beyond.
 DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
+  if (!par && pl.resident && 2 * b->d.nb <= 256 && !force_h8())
+    return launch_h8f(b, pl, list, count, n_hint, sol, eps, max_iters);
   if (2 * b->d.nb <= 512) {
     if (par) return pl.resident ? launch_h8<true, true>(b, pl, list, count, n_hint, sol, eps, max_iters)
                                 : launch_h8<true, false>(b, pl, list, count, n_hint, sol, eps, max_iters);
