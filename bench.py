@@ -406,7 +406,7 @@ def run_ours(args):
                              (B * 2 * (2 * T + 1) * NX * NX * 8 / 1e6)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "pcg_kernel<8,1,fast,resident>",
+                         "kernel": D.describe(prob),
                          "algorithmic_bytes_per_iteration": prof["pcg_bytes_per_iteration"],
                          "note": "blocks are SMEM-resident (TMA-staged once per solve), so algorithmic GB/s "
                                  "exceeds HBM; binding roofline is SMEM",

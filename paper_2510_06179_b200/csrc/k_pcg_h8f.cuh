@@ -45,6 +45,9 @@ __device__ __forceinline__ void load_rows(const double* blk, const Bases& bs, do
 
 }  // namespace h8f
 
+/// Dynamic shared memory of pcg_kernel_h8f (doubles).
+__host__ __device__ inline long h8f_smem_doubles(const Dims& d) { return d.blk_stride + 2L * (d.nb + 1) * 8 + 32; }
+
 template <int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __restrict__ work,
                                                      const int* __restrict__ n_work, int* __restrict__ counter,
@@ -61,12 +64,12 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
   const bool has_next = i + 1 < nb;
   const bool has_prev = i > 0;
   const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int rows = blockDim.x >> 1;  // padded block rows
+  const int nbuf = nb + 1;  // vector rows (row nb: read by the last row, masked)
 
   double* sblk = sm_pcg;
-  double* vbuf = sblk + d.blk_stride;  // [rows][8]
-  double* xbuf = vbuf + rows * 8;      // [rows][8]
-  double* red = xbuf + rows * 8;       // [64]
+  double* vbuf = sblk + d.blk_stride;  // [nbuf][8] x_i halves
+  double* xbuf = vbuf + nbuf * 8;      // [nbuf][8] hand-overs
+  double* red = xbuf + nbuf * 8;       // [32]: 8-slot partial areas (dot, norm)
 
   const int p = i & 1, m = (i >> 1) & 1;
   h8f::Bases bs;
@@ -82,26 +85,31 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
   const int max_iters = max_iters_cfg > 0 ? max_iters_cfg : 2 * nl;
   const double threshold = epsilon * epsilon;
 
-  auto dot = [&](const double* a, const double* b) -> double {
+  // block-wide dots: warp tree, then a fixed-order sum of the warp partials
+  // (the same value in every thread). `slot` selects one of the 8-entry
+  // partial areas so that back-to-back dots without a barrier between them
+  // never overwrite partials still being read.
+  auto partial = [&](const double* a, const double* b, int slot) {
     double s = fma(a[3], b[3], fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0])));
     s = act ? s : 0.0;
     s = warp_sum(s);
-    if (lane == 0) red[warp] = s;
-    __syncthreads();
-    double t = red[0];
-    for (int k = 1; k < nw; ++k) t = t + red[k];
+    if (lane == 0) red[slot * 8 + warp] = s;
+  };
+  auto total = [&](int slot) -> double {
+    double t = red[slot * 8];
+    for (int k = 1; k < nw; ++k) t = t + red[slot * 8 + k];
     return t;
+  };
+  auto dot = [&](const double* a, const double* b) -> double {
+    partial(a, b, 0);
+    __syncthreads();
+    return total(0);
   };
   auto norm = [&](const double* a) -> double {
     __syncthreads();
-    double s = fma(a[3], a[3], fma(a[2], a[2], fma(a[1], a[1], a[0] * a[0])));
-    s = act ? s : 0.0;
-    s = warp_sum(s);
-    if (lane == 0) red[32 + warp] = s;
+    partial(a, a, 2);
     __syncthreads();
-    double t = red[32];
-    for (int k = 1; k < nw; ++k) t = t + red[32 + k];
-    return sqrt(t);
+    return sqrt(total(2));
   };
 
   for (;;) {
@@ -132,11 +140,13 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
     const double* PuI = sblk + d.p_sup + io * 64;
     // vector rows in the vec_off layout (common.cuh): chunk k of row j sits at
     // j * 8 + 2 (k ^ ((j >> 1) & 3)); per-thread offsets of the chunks used
+    // (rows past the last one use its offsets; they never store)
     auto voff = [](int j, int k) { return j * 8 + 2 * (k ^ ((j >> 1) & 3)); };
-    const int my0 = voff(i, 2 * h), my1 = voff(i, 2 * h + 1);              // my half of row i
-    const int nx0 = voff(i + 1, 2 * h), nx1 = voff(i + 1, 2 * h + 1);      // ... of row i + 1
-    const int pv0 = voff(i - 1, 2 * h), pv1 = voff(i - 1, 2 * h + 1);      // ... of row i - 1
-    const int nf0 = voff(i + 1, 0), nf1 = voff(i + 1, 1), nf2 = voff(i + 1, 2), nf3 = voff(i + 1, 3);
+    const int iv = act ? i : nb - 1;
+    const int my0 = voff(iv, 2 * h), my1 = voff(iv, 2 * h + 1);            // my half of row i
+    const int nx0 = voff(iv + 1, 2 * h), nx1 = voff(iv + 1, 2 * h + 1);    // ... of row i + 1
+    const int pv0 = voff(iv - 1, 2 * h), pv1 = voff(iv - 1, 2 * h + 1);    // ... of row i - 1
+    const int nf0 = voff(iv + 1, 0), nf1 = voff(iv + 1, 1), nf2 = voff(iv + 1, 2), nf3 = voff(iv + 1, 3);
 
     double lam[4] = {0, 0, 0, 0}, r[4], pv[4], y[4];
     if (act) {
@@ -148,127 +158,108 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
     phase ^= 1;
     __syncthreads();
 
-    // out = A x, A = -S (D = S_ii, O = L_i = S_{i+1,i}) or Phi^-1 (D = P_ii, O = U_i = P_{i,i+1}).
-    auto matvec = [&](bool precond, const double* xr, double* out) {
+    // ---- building blocks of a product A x (A = -S: D = S_ii, O = L_i = S_{i+1,i};
+    //      A = Phi^-1: D = P_ii, O = U_i = P_{i,i+1}); 4-term partial sums for ILP
+    auto gather = [&](const double* xr, double* xf) {  // x_i in logical order
       double other[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) other[q] = __shfl_xor_sync(0xffffffffu, xr[q], 1);
-      double xf[8];  // x_i in logical order
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         xf[q] = h8f::sel(h, other[q], xr[q]);
         xf[4 + q] = h8f::sel(h, xr[q], other[q]);
       }
-      *reinterpret_cast<double2*>(vbuf + my0) = make_double2(xr[0], xr[1]);
-      *reinterpret_cast<double2*>(vbuf + my1) = make_double2(xr[2], xr[3]);
-
-      // own = D x_i, two 4-column partial sums per row
-      double2 dd[8][2];
-      h8f::load_rows(precond ? PdI : SdI, bs, dd);
-      double oa[4], ob[4];
-      oa[0] = dd[0][0].x * xf[0], oa[1] = dd[0][0].y * xf[0], oa[2] = dd[0][1].x * xf[0], oa[3] = dd[0][1].y * xf[0];
-      ob[0] = dd[4][0].x * xf[4], ob[1] = dd[4][0].y * xf[4], ob[2] = dd[4][1].x * xf[4], ob[3] = dd[4][1].y * xf[4];
+    };
+    auto rows_times = [&](const double2 (&m)[8][2], const double* xf, double* out) {  // my rows of M x
+      double a[4], b[4];
+      a[0] = m[0][0].x * xf[0], a[1] = m[0][0].y * xf[0], a[2] = m[0][1].x * xf[0], a[3] = m[0][1].y * xf[0];
+      b[0] = m[4][0].x * xf[4], b[1] = m[4][0].y * xf[4], b[2] = m[4][1].x * xf[4], b[3] = m[4][1].y * xf[4];
 #pragma unroll
       for (int c = 1; c < 4; ++c) {
-        oa[0] = fma(dd[c][0].x, xf[c], oa[0]);
-        oa[1] = fma(dd[c][0].y, xf[c], oa[1]);
-        oa[2] = fma(dd[c][1].x, xf[c], oa[2]);
-        oa[3] = fma(dd[c][1].y, xf[c], oa[3]);
-        ob[0] = fma(dd[4 + c][0].x, xf[4 + c], ob[0]);
-        ob[1] = fma(dd[4 + c][0].y, xf[4 + c], ob[1]);
-        ob[2] = fma(dd[4 + c][1].x, xf[4 + c], ob[2]);
-        ob[3] = fma(dd[4 + c][1].y, xf[4 + c], ob[3]);
+        a[0] = fma(m[c][0].x, xf[c], a[0]);
+        a[1] = fma(m[c][0].y, xf[c], a[1]);
+        a[2] = fma(m[c][1].x, xf[c], a[2]);
+        a[3] = fma(m[c][1].y, xf[c], a[3]);
+        b[0] = fma(m[4 + c][0].x, xf[4 + c], b[0]);
+        b[1] = fma(m[4 + c][0].y, xf[4 + c], b[1]);
+        b[2] = fma(m[4 + c][1].x, xf[4 + c], b[2]);
+        b[3] = fma(m[4 + c][1].y, xf[4 + c], b[3]);
       }
-      double own[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) own[q] = oa[q] + ob[q];
-
-      asm volatile("" ::: "memory");  // D is consumed: bound the live registers before O
-      double2 oo[8][2];
-      h8f::load_rows(precond ? PuI : SsI, bs, oo);
-      double hand[4];  // logical order, for block row i+1
-      if (precond) {   // U_i' x_i: half-column partial sums over my rows, partner completes
-        double part[8];
+      for (int q = 0; q < 4; ++q) out[q] = a[q] + b[q];
+    };
+    // my 4 entries of M' x given my rows xm of x: half-column partial sums
+    // over my rows, the partner lane completes the sums of my columns
+    auto trans_times = [&](const double2 (&m)[8][2], const double* xm, double* out) {
+      double part[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          part[c] = fma(oo[c][1].y, xr[3], fma(oo[c][1].x, xr[2], fma(oo[c][0].y, xr[1], oo[c][0].x * xr[0])));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double send = h8f::sel(h, part[q], part[4 + q]);
-          const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
-          hand[q] = h8f::sel(h, part[4 + q], part[q]) + recv;
-        }
-      } else {  // L_i x_i, my rows
-        double ha[4], hb[4];
-        ha[0] = oo[0][0].x * xf[0], ha[1] = oo[0][0].y * xf[0], ha[2] = oo[0][1].x * xf[0], ha[3] = oo[0][1].y * xf[0];
-        hb[0] = oo[4][0].x * xf[4], hb[1] = oo[4][0].y * xf[4], hb[2] = oo[4][1].x * xf[4], hb[3] = oo[4][1].y * xf[4];
-#pragma unroll
-        for (int c = 1; c < 4; ++c) {
-          ha[0] = fma(oo[c][0].x, xf[c], ha[0]);
-          ha[1] = fma(oo[c][0].y, xf[c], ha[1]);
-          ha[2] = fma(oo[c][1].x, xf[c], ha[2]);
-          ha[3] = fma(oo[c][1].y, xf[c], ha[3]);
-          hb[0] = fma(oo[4 + c][0].x, xf[4 + c], hb[0]);
-          hb[1] = fma(oo[4 + c][0].y, xf[4 + c], hb[1]);
-          hb[2] = fma(oo[4 + c][1].x, xf[4 + c], hb[2]);
-          hb[3] = fma(oo[4 + c][1].y, xf[4 + c], hb[3]);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) hand[q] = ha[q] + hb[q];
-      }
-      *reinterpret_cast<double2*>(xbuf + my0) = make_double2(hand[0], hand[1]);
-      *reinterpret_cast<double2*>(xbuf + my1) = make_double2(hand[2], hand[3]);
-      __syncthreads();
-
-      double up[4];  // logical order
-      if (!precond) {  // L_i' x_{i+1}: partial sums over my rows of x_{i+1}, partner completes
-        const double2 n0 = *reinterpret_cast<const double2*>(vbuf + nx0);
-        const double2 n1 = *reinterpret_cast<const double2*>(vbuf + nx1);
-        const double xn[4] = {n0.x, n0.y, n1.x, n1.y};
-        double part[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          part[c] = fma(oo[c][1].y, xn[3], fma(oo[c][1].x, xn[2], fma(oo[c][0].y, xn[1], oo[c][0].x * xn[0])));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double send = h8f::sel(h, part[q], part[4 + q]);
-          const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
-          up[q] = h8f::sel(h, part[4 + q], part[q]) + recv;
-        }
-      } else {  // U_i x_{i+1}, my rows
-        const double2 t0 = *reinterpret_cast<const double2*>(vbuf + nf0);
-        const double2 t1 = *reinterpret_cast<const double2*>(vbuf + nf1);
-        const double2 t2 = *reinterpret_cast<const double2*>(vbuf + nf2);
-        const double2 t3 = *reinterpret_cast<const double2*>(vbuf + nf3);
-        const double xn[8] = {t0.x, t0.y, t1.x, t1.y, t2.x, t2.y, t3.x, t3.y};
-        double ua[4], ub[4];
-        ua[0] = oo[0][0].x * xn[0], ua[1] = oo[0][0].y * xn[0], ua[2] = oo[0][1].x * xn[0], ua[3] = oo[0][1].y * xn[0];
-        ub[0] = oo[4][0].x * xn[4], ub[1] = oo[4][0].y * xn[4], ub[2] = oo[4][1].x * xn[4], ub[3] = oo[4][1].y * xn[4];
-#pragma unroll
-        for (int c = 1; c < 4; ++c) {
-          ua[0] = fma(oo[c][0].x, xn[c], ua[0]);
-          ua[1] = fma(oo[c][0].y, xn[c], ua[1]);
-          ua[2] = fma(oo[c][1].x, xn[c], ua[2]);
-          ua[3] = fma(oo[c][1].y, xn[c], ua[3]);
-          ub[0] = fma(oo[4 + c][0].x, xn[4 + c], ub[0]);
-          ub[1] = fma(oo[4 + c][0].y, xn[4 + c], ub[1]);
-          ub[2] = fma(oo[4 + c][1].x, xn[4 + c], ub[2]);
-          ub[3] = fma(oo[4 + c][1].y, xn[4 + c], ub[3]);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) up[q] = ua[q] + ub[q];
-      }
-      const double2 l0 = *reinterpret_cast<const double2*>(xbuf + pv0);
-      const double2 l1 = *reinterpret_cast<const double2*>(xbuf + pv1);
-      const double low[4] = {l0.x, l0.y, l1.x, l1.y};
-      // rows: diag, then sub (i > 0), then super (i < nb - 1)
+      for (int c = 0; c < 8; ++c)
+        part[c] = fma(m[c][1].y, xm[3], fma(m[c][1].x, xm[2], fma(m[c][0].y, xm[1], m[c][0].x * xm[0])));
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
+        const double send = h8f::sel(h, part[q], part[4 + q]);
+        const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+        out[q] = h8f::sel(h, part[4 + q], part[q]) + recv;
+      }
+    };
+    auto put = [&](double* buf, int o0, int o1, const double* x) {
+      if (act) {
+        *reinterpret_cast<double2*>(buf + o0) = make_double2(x[0], x[1]);
+        *reinterpret_cast<double2*>(buf + o1) = make_double2(x[2], x[3]);
+      }
+    };
+    auto get = [&](const double* buf, int o0, int o1, double* x) {
+      const double2 a = *reinterpret_cast<const double2*>(buf + o0);
+      const double2 b = *reinterpret_cast<const double2*>(buf + o1);
+      x[0] = a.x, x[1] = a.y, x[2] = b.x, x[3] = b.y;
+    };
+    // phase 1 for vector x (buffers vb, xb): publishes x_i and the hand-over
+    // for block row i+1, returns D_i x_i
+    auto phase1 = [&](bool precond, const double2 (&dd)[8][2], const double2 (&oo)[8][2], const double* xr,
+                      double* vb, double* xb, double* own) {
+      double xf[8];
+      gather(xr, xf);
+      put(vb, my0, my1, xr);
+      rows_times(dd, xf, own);
+      double hand[4];
+      if (precond) trans_times(oo, xr, hand);  // U_i' x_i
+      else rows_times(oo, xf, hand);            // L_i x_i
+      put(xb, my0, my1, hand);
+    };
+    // phase 2 (after the barrier): the sub term (hand-over of row i-1) and the super term
+    auto phase2 = [&](bool precond, const double2 (&oo)[8][2], const double* vb, const double* xb, double* low,
+                      double* up) {
+      if (!precond) {  // L_i' x_{i+1}
+        double xn[4];
+        get(vb, nx0, nx1, xn);
+        trans_times(oo, xn, up);
+      } else {  // U_i x_{i+1}
+        double xn[8];
+        get(vb, nf0, nf1, xn);
+        get(vb, nf2, nf3, xn + 4);
+        rows_times(oo, xn, up);
+      }
+      get(xb, pv0, pv1, low);
+    };
+    auto finish = [&](const double* own, const double* low, const double* up, double* out) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // diag, then sub (i > 0), then super (i < nb - 1)
         double acc = own[q];
         acc = has_prev ? acc + low[q] : acc;
         acc = has_next ? acc + up[q] : acc;
         out[q] = acc;
       }
+    };
+
+    auto matvec = [&](bool precond, const double* xr, double* out) {
+      double2 dd[8][2], oo[8][2];
+      h8f::load_rows(precond ? PdI : SdI, bs, dd);
+      h8f::load_rows(precond ? PuI : SsI, bs, oo);
+      double own[4], low[4], up[4];
+      phase1(precond, dd, oo, xr, vbuf, xbuf, own);
+      __syncthreads();
+      phase2(precond, oo, vbuf, xbuf, low, up);
+      finish(own, low, up, out);
     };
 
     matvec(false, lam, y);  // y = (-S) lambda0

@@ -27,11 +27,11 @@ int launch_h8(docp_batch* b, const PcgPlan& pl, const int* list, const int* coun
 }
 
 /// FAST with resident blocks: the instruction-lean pcg_kernel_h8f.
-int launch_h8f(docp_batch* b, const PcgPlan& pl, const int* list, const int* count, int n_hint, double* sol,
+int launch_h8f(docp_batch* b, const PcgPlan&, const int* list, const int* count, int n_hint, double* sol,
                double eps, int max_iters) {
   auto kern = pcg_kernel_h8f<256>;
+  const size_t smem = h8f_smem_doubles(b->d) * sizeof(double);
   const int threads = (2 * b->d.nb + 31) / 32 * 32;
-  const size_t smem = (static_cast<size_t>(b->d.blk_stride) + 2 * (threads / 2) * 8 + 64) * sizeof(double);
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
