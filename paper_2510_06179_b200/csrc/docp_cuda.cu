@@ -799,13 +799,18 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const bool res = pcg_smem(d, true) + 64 <= static_cast<size_t>(max_optin);
-  const char* fast = d.nx == 8 ? (res && 2 * d.nb <= 256 ? "pcg_kernel_h8f" : 2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
-                                : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>";
+  const int cl = h8f_cluster_for(d, dev);
+  char fast[64];
+  if (cl == 1) snprintf(fast, sizeof fast, "pcg_kernel_h8f(resident)");
+  else if (cl > 1) snprintf(fast, sizeof fast, "pcg_kernel_h8f(cluster%d,resident)", cl);
+  else snprintf(fast, sizeof fast, "%s", d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
+                                                   : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>");
   const char* parity = d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
                                   : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>";
-  return snprintf(buf, cap, "nx=%d layout=%s pcg=%s record=%ld B fast=%s parity=%s", d.nx,
-                  d.nx == 8 ? "swizzle8" : d.nx == 4 ? "swizzle4" : "colmajor", res ? "resident(TMA)" : "streaming",
-                  d.blk_stride * 8, fast, parity);
+  return snprintf(buf, cap, "nx=%d layout=%s record=%ld B parity=%s(%s) fast=%s", d.nx,
+                  d.nx == 8 ? "swizzle8" : d.nx == 4 ? "swizzle4" : "colmajor", d.blk_stride * 8, parity,
+                  res ? "resident" : "streaming", fast);
+
 }
 
 }  // extern "C"

@@ -16,7 +16,17 @@
 //    (selects, not multiplies, so garbage NaNs cannot leak);
 //  * every 8-term accumulation runs as two 4-term partial sums (ILP).
 // Vector rows keep the conflict-free vec_off layout, with per-thread offsets.
+//
+// CL > 1 (long horizons, T > 113): a thread-block cluster of CL CTAs solves
+// one problem; CTA c holds block rows [cR, cR + R) of every region in its own
+// shared memory (four TMA bulk copies), so the blocks stay on-chip however
+// long the horizon. Neighbour rows across a CTA boundary exchange x and the
+// hand-over through distributed shared memory (halo rows of vbuf / xbuf),
+// dot products gather every warp's partial in every CTA, and the barriers
+// become cluster barriers. CL = 1 is the single-CTA kernel.
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "k_pcg.cuh"
 
@@ -45,10 +55,23 @@ __device__ __forceinline__ void load_rows(const double* blk, const Bases& bs, do
 
 }  // namespace h8f
 
-/// Dynamic shared memory of pcg_kernel_h8f (doubles).
-__host__ __device__ inline long h8f_smem_doubles(const Dims& d) { return d.blk_stride + 2L * (d.nb + 1) * 8 + 32; }
+/// Block rows per CTA for a cluster of cl CTAs.
+__host__ __device__ inline int h8f_rows(const Dims& d, int cl) { return (d.nb + cl - 1) / cl; }
 
-template <int MAXT>
+/// Dynamic shared memory of pcg_kernel_h8f<*, CL> (doubles): four regions of
+/// R blocks, vbuf / xbuf with two halo rows, 3 x CL x 8 dot partials.
+__host__ __device__ inline long h8f_smem_doubles(const Dims& d, int cl) {
+  const long R = h8f_rows(d, cl);
+  return 4 * R * 64 + 2 * (R + 2) * 8 + 3L * cl * 8;
+}
+
+template <int CL>
+__device__ __forceinline__ void h8f_sync() {
+  if constexpr (CL == 1) __syncthreads();
+  else cooperative_groups::this_cluster().sync();
+}
+
+template <int MAXT, int CL>
 __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __restrict__ work,
                                                      const int* __restrict__ n_work, int* __restrict__ counter,
                                                      double* __restrict__ sol_all, double epsilon,
@@ -59,17 +82,25 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
   const Dims d = v.d;
   const int nl = d.nl, nb = d.nb;
   const int tid = threadIdx.x;
-  const int i = tid >> 1, h = tid & 1;
-  const bool act = i < nb;
-  const bool has_next = i + 1 < nb;
+  const int crank = CL == 1 ? 0 : static_cast<int>(cooperative_groups::this_cluster().block_rank());
+  const int R = h8f_rows(d, CL);               // block rows per CTA
+  const int row0 = crank * R;                  // first global block row of this CTA
+  const int nrows = max(0, min(R, nb - row0));  // block rows this CTA owns
+  const int nsub = max(0, min(R, nb - 1 - row0));  // ... that have an off-diagonal block
+  const int il = tid >> 1, h = tid & 1;
+  const int i = row0 + il;                     // global block row
+  const bool act = il < nrows;
+  const bool has_next = act && i + 1 < nb;
   const bool has_prev = i > 0;
   const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int nbuf = nb + 1;  // vector rows (row nb: read by the last row, masked)
 
-  double* sblk = sm_pcg;
-  double* vbuf = sblk + d.blk_stride;  // [nbuf][8] x_i halves
-  double* xbuf = vbuf + nbuf * 8;      // [nbuf][8] hand-overs
-  double* red = xbuf + nbuf * 8;       // [32]: 8-slot partial areas (dot, norm)
+  double* sSd = sm_pcg;            // [R] blocks
+  double* sSs = sSd + R * 64;      // [R]
+  double* sPd = sSs + R * 64;      // [R]
+  double* sPu = sPd + R * 64;      // [R]
+  double* vbuf = sPu + R * 64;     // [R + 2] x_i halves; slot = local row + 1, slots 0 / R+1 are halos
+  double* xbuf = vbuf + (R + 2) * 8;  // [R + 2] hand-overs
+  double* red = xbuf + (R + 2) * 8;   // [3][CL][8] dot partials
 
   const int p = i & 1, m = (i >> 1) & 1;
   h8f::Bases bs;
@@ -85,68 +116,98 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
   const int max_iters = max_iters_cfg > 0 ? max_iters_cfg : 2 * nl;
   const double threshold = epsilon * epsilon;
 
-  // block-wide dots: warp tree, then a fixed-order sum of the warp partials
-  // (the same value in every thread). `slot` selects one of the 8-entry
-  // partial areas so that back-to-back dots without a barrier between them
-  // never overwrite partials still being read.
+  // block-wide (cluster-wide) dots: warp tree, every warp's partial stored in
+  // every CTA of the cluster, one barrier, then the same fixed-order sum in
+  // every thread. `slot` selects one of three partial areas so that dots
+  // without a barrier between them never overwrite partials still being read.
   auto partial = [&](const double* a, const double* b, int slot) {
     double s = fma(a[3], b[3], fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0])));
     s = act ? s : 0.0;
     s = warp_sum(s);
-    if (lane == 0) red[slot * 8 + warp] = s;
+    if (lane == 0) {
+      const int at = (slot * CL + crank) * 8 + warp;
+      if constexpr (CL == 1) {
+        red[at] = s;
+      } else {
+#pragma unroll
+        for (int c = 0; c < CL; ++c) cooperative_groups::this_cluster().map_shared_rank(red, c)[at] = s;
+      }
+    }
   };
   auto total = [&](int slot) -> double {
-    double t = red[slot * 8];
-    for (int k = 1; k < nw; ++k) t = t + red[slot * 8 + k];
+    double t = red[slot * CL * 8];
+    for (int k = 1; k < CL * 8; ++k)
+      if ((k & 7) < nw) t = t + red[slot * CL * 8 + k];
     return t;
   };
   auto dot = [&](const double* a, const double* b) -> double {
     partial(a, b, 0);
-    __syncthreads();
+    h8f_sync<CL>();
     return total(0);
   };
   auto norm = [&](const double* a) -> double {
-    __syncthreads();
+    h8f_sync<CL>();
     partial(a, a, 2);
-    __syncthreads();
+    h8f_sync<CL>();
     return sqrt(total(2));
   };
 
   for (;;) {
-    if (tid == 0) s_work = atomicAdd(counter, 1);
-    __syncthreads();
+    if (tid == 0 && crank == 0) {
+      const int wk = atomicAdd(counter, 1);
+      if constexpr (CL == 1) {
+        s_work = wk;
+      } else {
+#pragma unroll
+        for (int c = 0; c < CL; ++c) *cooperative_groups::this_cluster().map_shared_rank(&s_work, c) = wk;
+      }
+    }
+    h8f_sync<CL>();
     const int w = s_work;
     if (w >= *n_work) break;
     const int pidx = work[w];
     if (v.status[pidx].code != DOCP_OK) {
-      __syncthreads();
+      h8f_sync<CL>();
       continue;
     }
     const double* rec = v.blocks + static_cast<long>(pidx) * d.blk_stride;
-    if (tid == 0) {
+    if (tid == 0) {  // this CTA's rows of the four regions
       fence_proxy_async();
-      const uint32_t bytes = static_cast<uint32_t>((d.p_sup + ((static_cast<long>(d.T) * d.bsz + 1) & ~1L)) * 8);
-      mbar_arrive_expect_tx(&s_bar, bytes);
-      tma_bulk_g2s(sblk, rec, bytes, &s_bar);
+      const uint32_t bd = static_cast<uint32_t>(nrows) * 512u, bo = static_cast<uint32_t>(nsub) * 512u;
+      mbar_arrive_expect_tx(&s_bar, 2 * bd + 2 * bo);
+      if (bd) {
+        tma_bulk_g2s(sSd, rec + d.s_diag + row0 * 64, bd, &s_bar);
+        tma_bulk_g2s(sPd, rec + d.p_diag + row0 * 64, bd, &s_bar);
+      }
+      if (bo) {
+        tma_bulk_g2s(sSs, rec + d.s_sub + row0 * 64, bo, &s_bar);
+        tma_bulk_g2s(sPu, rec + d.p_sup + row0 * 64, bo, &s_bar);
+      }
     }
     const double* gam = v.gamma + static_cast<long>(pidx) * nl;
     double* sol = sol_all + static_cast<long>(pidx) * nl;
-    // this thread's blocks (rows past the last one reuse its blocks; masked below)
-    const int ib = act ? i : nb - 1;
-    const int io = has_next ? i : 0;
-    const double* SdI = sblk + d.s_diag + ib * 64;
-    const double* PdI = sblk + d.p_diag + ib * 64;
-    const double* SsI = sblk + d.s_sub + io * 64;
-    const double* PuI = sblk + d.p_sup + io * 64;
-    // vector rows in the vec_off layout (common.cuh): chunk k of row j sits at
+    // this thread's blocks (rows past the last one reuse a valid block; masked below)
+    const int ib = act ? il : max(0, nrows - 1);
+    const int io = has_next ? il : 0;
+    const double* SdI = sSd + ib * 64;
+    const double* PdI = sPd + ib * 64;
+    const double* SsI = sSs + io * 64;
+    const double* PuI = sPu + io * 64;
+    // vector slots in the vec_off layout (common.cuh): chunk k of slot j sits at
     // j * 8 + 2 (k ^ ((j >> 1) & 3)); per-thread offsets of the chunks used
     // (rows past the last one use its offsets; they never store)
     auto voff = [](int j, int k) { return j * 8 + 2 * (k ^ ((j >> 1) & 3)); };
-    const int iv = act ? i : nb - 1;
-    const int my0 = voff(iv, 2 * h), my1 = voff(iv, 2 * h + 1);            // my half of row i
-    const int nx0 = voff(iv + 1, 2 * h), nx1 = voff(iv + 1, 2 * h + 1);    // ... of row i + 1
-    const int pv0 = voff(iv - 1, 2 * h), pv1 = voff(iv - 1, 2 * h + 1);    // ... of row i - 1
-    const int nf0 = voff(iv + 1, 0), nf1 = voff(iv + 1, 1), nf2 = voff(iv + 1, 2), nf3 = voff(iv + 1, 3);
+    const int sv = (act ? il : max(0, nrows - 1)) + 1;  // my slot
+    const int my0 = voff(sv, 2 * h), my1 = voff(sv, 2 * h + 1);            // my half of row i
+    const int nx0 = voff(sv + 1, 2 * h), nx1 = voff(sv + 1, 2 * h + 1);    // ... of row i + 1
+    const int pv0 = voff(sv - 1, 2 * h), pv1 = voff(sv - 1, 2 * h + 1);    // ... of row i - 1
+    const int nf0 = voff(sv + 1, 0), nf1 = voff(sv + 1, 1), nf2 = voff(sv + 1, 2), nf3 = voff(sv + 1, 3);
+    // halo targets in the neighbours: my x half -> slot R+1 of CTA c-1 (first row),
+    // my hand-over -> slot 0 of CTA c+1 (last row)
+    const bool to_prev = CL > 1 && act && il == 0 && crank > 0;
+    const bool to_next = CL > 1 && act && il == R - 1 && crank < CL - 1;
+    const int hx0 = voff(R + 1, 2 * h), hx1 = voff(R + 1, 2 * h + 1);
+    const int hh0 = voff(0, 2 * h), hh1 = voff(0, 2 * h + 1);
 
     double lam[4] = {0, 0, 0, 0}, r[4], pv[4], y[4];
     if (act) {
@@ -220,11 +281,23 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       double xf[8];
       gather(xr, xf);
       put(vb, my0, my1, xr);
+      if constexpr (CL > 1)
+        if (to_prev) {
+          double* rv = cooperative_groups::this_cluster().map_shared_rank(vb, crank - 1);
+          *reinterpret_cast<double2*>(rv + hx0) = make_double2(xr[0], xr[1]);
+          *reinterpret_cast<double2*>(rv + hx1) = make_double2(xr[2], xr[3]);
+        }
       rows_times(dd, xf, own);
       double hand[4];
       if (precond) trans_times(oo, xr, hand);  // U_i' x_i
       else rows_times(oo, xf, hand);            // L_i x_i
       put(xb, my0, my1, hand);
+      if constexpr (CL > 1)
+        if (to_next) {
+          double* rx = cooperative_groups::this_cluster().map_shared_rank(xb, crank + 1);
+          *reinterpret_cast<double2*>(rx + hh0) = make_double2(hand[0], hand[1]);
+          *reinterpret_cast<double2*>(rx + hh1) = make_double2(hand[2], hand[3]);
+        }
     };
     // phase 2 (after the barrier): the sub term (hand-over of row i-1) and the super term
     auto phase2 = [&](bool precond, const double2 (&oo)[8][2], const double* vb, const double* xb, double* low,
@@ -257,7 +330,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       h8f::load_rows(precond ? PuI : SsI, bs, oo);
       double own[4], low[4], up[4];
       phase1(precond, dd, oo, xr, vbuf, xbuf, own);
-      __syncthreads();
+      h8f_sync<CL>();
       phase2(precond, oo, vbuf, xbuf, low, up);
       finish(own, low, up, out);
     };
@@ -270,7 +343,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
     } else {
       r[0] = r[1] = r[2] = r[3] = 0.0;
     }
-    __syncthreads();  // every phase-2 read of lambda / its hand-over is done
+    h8f_sync<CL>();  // every phase-2 read of lambda / its hand-over is done
     matvec(true, r, pv);  // r~
     double eta = dot(r, pv);
     int status = DOCP_OK, iters = 0;
@@ -315,7 +388,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       *reinterpret_cast<double2*>(sol + i * 8 + 4 * h) = make_double2(lam[0], lam[1]);
       *reinterpret_cast<double2*>(sol + i * 8 + 4 * h + 2) = make_double2(lam[2], lam[3]);
     }
-    if (tid == 0) {
+    if (tid == 0 && crank == 0) {
       v.pcg_iters[pidx] = iters;
       v.final_eta[pidx] = eta;
       v.pcg_conv[pidx] = status == DOCP_OK && eta <= threshold;
@@ -325,7 +398,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       atomicAdd(v.pcg_acc + 1, 1ull);
       atomicAdd(v.pcg_acc + 2, 1ull);  // lifetime solves (docp_pcg_invocations)
     }
-    __syncthreads();
+    h8f_sync<CL>();
   }
 }
 

@@ -26,23 +26,58 @@ int launch_h8(docp_batch* b, const PcgPlan& pl, const int* list, const int* coun
   return DOCP_OK;
 }
 
-/// FAST with resident blocks: the instruction-lean pcg_kernel_h8f.
-int launch_h8f(docp_batch* b, const PcgPlan&, const int* list, const int* count, int n_hint, double* sol,
-               double eps, int max_iters) {
-  auto kern = pcg_kernel_h8f<256>;
-  const size_t smem = h8f_smem_doubles(b->d) * sizeof(double);
-  const int threads = (2 * b->d.nb + 31) / 32 * 32;
+/// FAST: the instruction-lean pcg_kernel_h8f, on a cluster of cl CTAs
+/// (cl = 1: one CTA per problem; cl > 1: the problem's block rows split over
+/// the cluster's shared memories).
+template <int CL>
+int launch_h8f_cl(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
+                  int max_iters) {
+  auto kern = pcg_kernel_h8f<256, CL>;
+  const size_t smem = h8f_smem_doubles(b->d, CL) * sizeof(double);
+  const int threads = (2 * h8f_rows(b->d, CL) + 31) / 32 * 32;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit on an SM (smem %zu)", smem);
-  const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
+  cudaLaunchConfig_t lc{};
+  cudaLaunchAttribute attr[1];
+  lc.blockDim = dim3(threads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = b->stream;
+  int groups = 0;  // concurrently resident clusters (CTAs for CL = 1)
+  if (CL == 1) {
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    groups = per_sm * b->num_sms;
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    lc.gridDim = dim3(CL * b->num_sms);
+    CUDA_TRY(cudaOccupancyMaxActiveClusters(&groups, kern, &lc));
+  }
+  if (groups < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit (cluster %d, smem %zu)", CL, smem);
+  lc.gridDim = dim3(CL * std::max(1, std::min(n_hint, groups)));
   CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
   ProfScope ps(b, DOCP_PROF_PCG);
-  kern<<<grid, threads, smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
+  CUDA_TRY(cudaLaunchKernelEx(&lc, kern, b->v, list, count, b->counts + 3, sol, eps, max_iters));
   LAUNCH_CHECK();
   return DOCP_OK;
 }
+
+/// Smallest cluster (1, 2, 4, 8) whose per-CTA share of the blocks fits in
+/// shared memory with at most 128 block rows per CTA; 0 if none.
+int h8f_cluster_for(const Dims& d, int device) {
+  if (d.nx != 8) return 0;
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  for (int cl : {1, 2, 4, 8}) {
+    if (cl > 1 && (cl - 1) * h8f_rows(d, cl) >= d.nb) break;  // every CTA must own a row
+    if (h8f_rows(d, cl) <= 128 && h8f_smem_doubles(d, cl) * 8 + 64 <= static_cast<long>(max_optin)) return cl;
+  }
+  return 0;
+}
+static int h8f_cluster(const docp_batch* b) { return h8f_cluster_for(b->d, b->device); }
 
 /// Kernel variant override for A/B measurements: DOCP_PCG_VARIANT=h8 keeps
 /// FAST solves on pcg_kernel_h8.
@@ -51,12 +86,19 @@ static bool force_h8() {
   return e && std::strcmp(e, "h8") == 0;
 }
 
-/// n_x = 8: FAST + resident blocks -> pcg_kernel_h8f; otherwise two threads
-/// per block row (pcg_kernel_h8) up to T = 255, one thread per block row
-/// (pcg_kernel) beyond.
+/// n_x = 8: FAST -> pcg_kernel_h8f on the smallest cluster that keeps the
+/// blocks on-chip; PARITY (or no fitting cluster): two threads per block row
+/// (pcg_kernel_h8) up to T = 255, one thread per block row (pcg_kernel) beyond.
 DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
-  if (!par && pl.resident && 2 * b->d.nb <= 256 && !force_h8())
-    return launch_h8f(b, pl, list, count, n_hint, sol, eps, max_iters);
+  if (!par && !force_h8()) {
+    switch (h8f_cluster(b)) {
+      case 1: return launch_h8f_cl<1>(b, list, count, n_hint, sol, eps, max_iters);
+      case 2: return launch_h8f_cl<2>(b, list, count, n_hint, sol, eps, max_iters);
+      case 4: return launch_h8f_cl<4>(b, list, count, n_hint, sol, eps, max_iters);
+      case 8: return launch_h8f_cl<8>(b, list, count, n_hint, sol, eps, max_iters);
+      default: break;
+    }
+  }
   if (2 * b->d.nb <= 512) {
     if (par) return pl.resident ? launch_h8<true, true>(b, pl, list, count, n_hint, sol, eps, max_iters)
                                 : launch_h8<true, false>(b, pl, list, count, n_hint, sol, eps, max_iters);

@@ -129,7 +129,9 @@ def test_pcg_breakdown_and_cap(D):
 
 
 @pytest.mark.parametrize("nx,nu,T,seed", [(4, 2, 10, 1), (8, 4, 30, 2), (8, 4, 100, 3), (6, 3, 12, 4),
-                                          (16, 8, 30, 5), (9, 2, 40, 6)])
+                                          (16, 8, 30, 5), (9, 2, 40, 6), (8, 4, 4, 7),
+                                          # long horizons: FAST runs on a 2-, 4- and 8-CTA cluster
+                                          (8, 4, 128, 8), (8, 4, 256, 9), (8, 4, 500, 10)])
 def test_pcg_on_oracle_blocks(D, nx, nu, T, seed):
     """K2 alone: blocks and gamma assembled by the oracle; PARITY is
     bit-identical to the oracle's pcg_solve, FAST within 1e-9 with equal
