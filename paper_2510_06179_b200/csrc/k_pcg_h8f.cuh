@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
                                                      double* __restrict__ sol_all, double epsilon,
                                                      int max_iters_cfg) {
   extern __shared__ __align__(128) double sm_pcg[];
-  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ __align__(8) uint64_t s_bar[2];  // [0]: -S blocks, [1]: Phi^-1 blocks
   __shared__ int s_work;
   const Dims d = v.d;
   const int nl = d.nl, nb = d.nb;
@@ -110,7 +110,10 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
     for (int j = 0; j < 2; ++j)
       bs.o[k][j] = ((k & 1) ? -8 * p : 8 * p) + 4 * ((k >> 1) ? 1 - h : h) + 2 * (j ^ m);
 
-  if (tid == 0) mbar_init(&s_bar, 1);
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+  }
   __syncthreads();
   uint32_t phase = 0;
   const int max_iters = max_iters_cfg > 0 ? max_iters_cfg : 2 * nl;
@@ -174,15 +177,14 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
     if (tid == 0) {  // this CTA's rows of the four regions
       fence_proxy_async();
       const uint32_t bd = static_cast<uint32_t>(nrows) * 512u, bo = static_cast<uint32_t>(nsub) * 512u;
-      mbar_arrive_expect_tx(&s_bar, 2 * bd + 2 * bo);
-      if (bd) {
-        tma_bulk_g2s(sSd, rec + d.s_diag + row0 * 64, bd, &s_bar);
-        tma_bulk_g2s(sPd, rec + d.p_diag + row0 * 64, bd, &s_bar);
-      }
-      if (bo) {
-        tma_bulk_g2s(sSs, rec + d.s_sub + row0 * 64, bo, &s_bar);
-        tma_bulk_g2s(sPu, rec + d.p_sup + row0 * 64, bo, &s_bar);
-      }
+      // -S first on its own barrier: the first product only needs those blocks,
+      // so it starts while the Phi^-1 half is still in flight
+      mbar_arrive_expect_tx(&s_bar[0], bd + bo);
+      mbar_arrive_expect_tx(&s_bar[1], bd + bo);
+      if (bd) tma_bulk_g2s(sSd, rec + d.s_diag + row0 * 64, bd, &s_bar[0]);
+      if (bo) tma_bulk_g2s(sSs, rec + d.s_sub + row0 * 64, bo, &s_bar[0]);
+      if (bd) tma_bulk_g2s(sPd, rec + d.p_diag + row0 * 64, bd, &s_bar[1]);
+      if (bo) tma_bulk_g2s(sPu, rec + d.p_sup + row0 * 64, bo, &s_bar[1]);
     }
     const double* gam = v.gamma + static_cast<long>(pidx) * nl;
     double* sol = sol_all + static_cast<long>(pidx) * nl;
@@ -215,9 +217,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       const double2 b = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h + 2);
       lam[0] = a.x, lam[1] = a.y, lam[2] = b.x, lam[3] = b.y;
     }
-    mbar_wait(&s_bar, phase);
-    phase ^= 1;
-    __syncthreads();
+    mbar_wait(&s_bar[0], phase);
 
     // ---- building blocks of a product A x (A = -S: D = S_ii, O = L_i = S_{i+1,i};
     //      A = Phi^-1: D = P_ii, O = U_i = P_{i,i+1}); 4-term partial sums for ILP
@@ -344,6 +344,8 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       r[0] = r[1] = r[2] = r[3] = 0.0;
     }
     h8f_sync<CL>();  // every phase-2 read of lambda / its hand-over is done
+    mbar_wait(&s_bar[1], phase);
+    phase ^= 1;
     matvec(true, r, pv);  // r~
     double eta = dot(r, pv);
     int status = DOCP_OK, iters = 0;
