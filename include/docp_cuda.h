@@ -18,6 +18,8 @@
  *                             Z/LAMBDA fields hold the warm-start cache)
  *   docp_backward_vjp     <- docp::backward_vjp     backward.hpp:27-50
  *   docp_il_epoch         <- the train_il epoch body train.hpp:82-131
+ *   docp_rollout          <- docp::rollout          batch.hpp:172-212 (affine env, train.hpp:195-213)
+ *   docp_rollout_backward <- docp::rollout_backward batch.hpp:221-258
  *   docp_pcg_invocations  <- docp::stats::pcg_invocations common.hpp:112-115
  *
  * Callbacks (OcpDefinition's std::functions, problem.hpp:43-54) cannot cross
@@ -82,14 +84,16 @@ enum docp_where {
   DOCP_AT_MERIT_STATE = 10,  /* sqp.hpp:104-106 */
   DOCP_AT_MERIT_CONTROL = 11,
   DOCP_AT_SQP_ITERATE = 12,  /* sqp.hpp:240-243 */
-  DOCP_AT_INITIAL_GUESS = 13 /* sqp.hpp:220-221 */
+  DOCP_AT_INITIAL_GUESS = 13, /* sqp.hpp:220-221 */
+  DOCP_AT_ROLLOUT_ENV = 14    /* batch.hpp:195-199: environment produced a non-finite state at step index */
 };
 
 typedef struct docp_status {
   int32_t code;  /* docp_code */
   int32_t where; /* docp_where */
   int32_t index; /* stage, PCG iteration (BreakdownError::iteration) or SQP iteration */
-  int32_t reserved;
+  int32_t step;  /* rollout statuses: 1 + the episode step a solve failed at (RolloutTruncation,
+                    batch.hpp:186-191; formatted as "rollout: solve failed at step k: ..."), else 0 */
 } docp_status;
 
 typedef struct docp_problem {
@@ -147,7 +151,9 @@ enum docp_field {
   DOCP_F_ALPHA = 19,       /* [B] double, last line-search alpha */
   DOCP_F_ACCEPTED = 20,    /* [B] int32, last line-search accepted flag */
   DOCP_F_LOSS = 21,        /* [B] double, per-instance IL loss */
-  DOCP_F_COUNT = 22
+  DOCP_F_ROLLOUT_STATUS = 22, /* [B] docp_status of the last rollout (+ its backward) */
+  DOCP_F_REWARD = 23,      /* [B] double, total reward of the last rollout */
+  DOCP_F_COUNT = 24
 };
 
 typedef struct docp_batch docp_batch;
@@ -210,6 +216,21 @@ int docp_backward_vjp(docp_batch* batch, const docp_pcg_config* cfg);
 int docp_il_epoch(docp_batch* batch, const docp_sqp_config* cfg, const double* weights, int32_t learn_start,
                   int32_t learn_size, const double* demos, double loss_denominator, double* loss_sum,
                   double* grad_sum);
+
+/* Closed-loop MPC rollouts (batch.hpp:172-212) of affine-quadratic instances
+ * with their own dynamics as the environment and reward -(|x'|^2 + |u|^2)
+ * (make_affine_env, train.hpp:195-213). For each instance: the initial-state
+ * segment of THETA is set to the current state, the problem is solved warm-
+ * started from the previous step (Z, LAMBDA; zero at step 0), the first
+ * control is applied, the reward accumulated. x_init: device [B][n_x].
+ * Per-instance truncations go to ROLLOUT_STATUS; REWARD receives the totals.
+ * Every step's solution is recorded on the device for docp_rollout_backward. */
+int docp_rollout(docp_batch* batch, const docp_sqp_config* cfg, const double* x_init, int32_t episode_length);
+/* rollout_backward (batch.hpp:221-258) of the last rollout: GRAD_THETA <-
+ * dJ/dtheta of the total reward, its initial-state segment = dJ/dx_init.
+ * The adjoint multiplier is chained across steps; instances whose rollout
+ * was truncated are skipped (their ROLLOUT_STATUS is not OK). */
+int docp_rollout_backward(docp_batch* batch, const docp_pcg_config* cfg);
 
 /* ---- synthetic inputs (the reference generators' recipe, generators.hpp) -- */
 /* count sequential random_convex_instance (convex != 0) / random_linear_instance

@@ -154,6 +154,9 @@ def load(kind: str):
             lib.ref_spectral_radius.restype = C.c_double
             lib.ref_spectral_radius.argtypes = [dp, C.c_int]
             lib.ref_pcg_invocations.restype = C.c_ulonglong
+            lib.ref_rollout_affine.restype = C.c_int
+            lib.ref_rollout_affine.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int,
+                                               C.POINTER(SqpConfig), dp, dp, ip, C.c_char_p]
         _loaded[kind] = lib
     return _loaded[kind]
 
@@ -341,6 +344,21 @@ def gen_aq(nx, nu, T, seed, count, convex=True):
     th = np.zeros((count, nx + nu + nx * nx + nx * nu + 2 * nx))
     lib.ref_gen_aq(nx, nu, T, seed, count, 1 if convex else 0, _p(th))
     return th
+
+
+def rollout_affine(nx, nu, T, thetas, x_inits, episode_length, cfg):
+    """The reference's rollout + rollout_backward per instance (ref only):
+    (rewards, grads, ok, messages)."""
+    lib = load("ref")
+    B = thetas.shape[0]
+    rewards, grads = np.zeros(B), np.zeros_like(np.asarray(thetas, np.float64))
+    ok = np.zeros(B, np.int32)
+    msgs = C.create_string_buffer(256 * B)
+    lib.ref_rollout_affine(nx, nu, T, B, _p(_arr(thetas)), _p(_arr(x_inits)), episode_length, C.byref(cfg),
+                           _p(rewards), _p(grads), ok.ctypes.data_as(C.POINTER(C.c_int)), msgs)
+    raw = msgs.raw
+    messages = [raw[256 * j:256 * (j + 1)].split(b"\0")[0].decode() for j in range(B)]
+    return rewards, grads, ok.astype(bool), messages
 
 
 def gen_cartpole(seed, horizon, n_demos):

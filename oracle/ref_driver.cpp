@@ -441,6 +441,46 @@ int ref_train_il_cartpole(std::uint64_t seed, int horizon, int n_demos, const do
   return 0;
 }
 
+/// rollout + rollout_backward (batch.hpp:172-258) of affine-quadratic
+/// instances with their own dynamics as the environment (make_affine_env,
+/// train.hpp:195-213): the train_rl inner body (train.hpp:287-297), one
+/// instance per theta row, x_init per row. ok[j] = 0 with the exception text
+/// in messages[j * 256] when the reference throws for that instance.
+int ref_rollout_affine(int nx, int nu, int horizon, int batch, const double* thetas, const double* x_inits,
+                       int episode_length, const port_sqp_config* c, double* rewards, double* grads, int* ok,
+                       char* messages) {
+  const std::size_t nth = static_cast<std::size_t>(nx + nu + nx * nx + nx * nu + nx + nx);
+  SqpConfig cfg = make_cfg(*c);
+  parallel_for(static_cast<std::size_t>(batch), 0, [&](std::size_t j) {
+    const double* th = thetas + j * nth;
+    AffineQuadratic p;
+    p.n_x = nx;
+    p.n_u = nu;
+    p.horizon = horizon;
+    p.w_x = vec(th, nx);
+    p.w_u = vec(th + nx, nu);
+    p.A = Eigen::Map<const Matrix>(th + nx + nu, nx, nx);
+    p.B = Eigen::Map<const Matrix>(th + nx + nu + nx * nx, nx, nu);
+    p.b_affine = vec(th + nx + nu + nx * nx + nx * nu, nx);
+    p.x_s = vec(th + nx + nu + nx * nx + nx * nu + nx, nx);
+    OcpDefinition ocp = p.make_ocp();
+    ParameterVector theta = p.make_theta();
+    DiffEnv env = bench::make_affine_env(p);
+    try {
+      RolloutOutput roll = rollout(env, ocp, theta, vec(x_inits + j * static_cast<std::size_t>(nx), nx),
+                                   episode_length, cfg);
+      Vector g = rollout_backward(roll.record, env, ocp, theta, cfg.pcg);
+      rewards[j] = roll.total_reward;
+      put(g, grads + j * nth);
+      ok[j] = 1;
+    } catch (const Error& e) {
+      ok[j] = 0;
+      std::snprintf(messages + j * 256, 256, "%s", e.what());
+    }
+  });
+  return 0;
+}
+
 /// bench::gen_cartpole (generators.hpp:134-168): initial states (n x 4) and
 /// expert demonstrations (n x n_z, flat layout).
 int ref_gen_cartpole(std::uint64_t seed, int horizon, int n_demos, double* x0s, double* demos, port_status* st) {

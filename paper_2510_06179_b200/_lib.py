@@ -20,7 +20,8 @@ MAX_STEP_CANDIDATES = 8
 
 (F_THETA, F_Z, F_LAMBDA, F_LAMBDA_TILDE, F_LOSS_GRAD_Z, F_GRAD_THETA, F_GAMMA, F_Z_QP, F_STATUS, F_SQP_ITERS,
  F_CONVERGED, F_KKT, F_PCG_ITERS, F_PCG_CONVERGED, F_FINAL_ETA, F_PCG_HISTORY, F_STEP_SIZES, F_PD_PROJECTED, F_MU,
- F_ALPHA, F_ACCEPTED, F_LOSS) = range(22)
+ F_ALPHA, F_ACCEPTED, F_LOSS, F_ROLLOUT_STATUS, F_REWARD) = range(24)
+AT_ROLLOUT_ENV = 14
 
 
 class Problem(C.Structure):
@@ -30,7 +31,7 @@ class Problem(C.Structure):
 
 
 class Status(C.Structure):
-    _fields_ = [("code", C.c_int32), ("where", C.c_int32), ("index", C.c_int32), ("reserved", C.c_int32)]
+    _fields_ = [("code", C.c_int32), ("where", C.c_int32), ("index", C.c_int32), ("step", C.c_int32)]
 
 
 class PcgConfigC(C.Structure):
@@ -83,6 +84,8 @@ SIGNATURES = {
     "docp_sqp_solve": (C.c_int, [_vp, C.POINTER(SqpConfigC)]),
     "docp_backward_vjp": (C.c_int, [_vp, C.POINTER(PcgConfigC)]),
     "docp_il_epoch": (C.c_int, [_vp, C.POINTER(SqpConfigC), _vp, _i32, _i32, _vp, _dbl, _vp, _vp]),
+    "docp_rollout": (C.c_int, [_vp, C.POINTER(SqpConfigC), _vp, _i32]),
+    "docp_rollout_backward": (C.c_int, [_vp, C.POINTER(PcgConfigC)]),
     "docp_generate_affine_quadratic": (C.c_int, [_i32, _i32, _u64, _i32, _i32, _dp]),
     "docp_generate_uniform": (C.c_int, [_u64, _i32, _dbl, _dbl, _dp]),
     "docp_generate_cartpole_x0": (C.c_int, [_u64, _i32, _dp]),

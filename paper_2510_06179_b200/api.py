@@ -58,6 +58,14 @@ class DivergenceError(Error):
     """Iterates became non-finite."""
 
 
+class RolloutTruncation(Error):
+    """A rollout abandoned because a solve failed mid-episode (batch.hpp:146-153)."""
+
+    def __init__(self, msg, step):
+        super().__init__(msg)
+        self.step = step
+
+
 class CudaError(Error):
     """The CUDA runtime or the ABI rejected a call."""
 
@@ -81,6 +89,10 @@ def status_error(st: L.Status) -> Optional[Error]:
     buf = C.create_string_buffer(256)
     L.lib().docp_format_status(C.byref(st), buf, 256)
     msg = buf.value.decode()
+    if st.step > 0:
+        return RolloutTruncation(msg, st.step - 1)
+    if st.where == L.AT_ROLLOUT_ENV:
+        return RolloutTruncation(msg, st.index)
     if st.code == L.BREAKDOWN:
         return BreakdownError(msg, st.index)
     return _BY_CODE.get(st.code, Error)(msg)
@@ -208,7 +220,7 @@ def generate_cartpole_x0(seed: int, n: int) -> np.ndarray:
 # --------------------------------------------------------------------------- batch
 
 _FLOAT_FIELDS = {L.F_THETA, L.F_Z, L.F_LAMBDA, L.F_LAMBDA_TILDE, L.F_LOSS_GRAD_Z, L.F_GRAD_THETA, L.F_GAMMA,
-                 L.F_Z_QP, L.F_KKT, L.F_FINAL_ETA, L.F_STEP_SIZES, L.F_MU, L.F_ALPHA, L.F_LOSS}
+                 L.F_Z_QP, L.F_KKT, L.F_FINAL_ETA, L.F_STEP_SIZES, L.F_MU, L.F_ALPHA, L.F_LOSS, L.F_REWARD}
 
 
 class Batch:
@@ -251,7 +263,7 @@ class Batch:
 
     def download(self, f: int) -> np.ndarray:
         _, n = self.field_ptr(f)
-        if f == L.F_STATUS:
+        if f in (L.F_STATUS, L.F_ROLLOUT_STATUS):
             arr = np.zeros((self.B, 4), np.int32)
         else:
             dtype = np.float64 if f in _FLOAT_FIELDS else np.int32
@@ -348,6 +360,22 @@ class Batch:
         c = cfg.c()
         _raise_call(L.lib().docp_il_epoch(self.h, C.byref(c), weights_ptr, learn_start, learn_size, demos_ptr,
                                           loss_denominator, loss_sum_ptr, grad_sum_ptr))
+
+
+    def rollout(self, cfg: SqpConfig, x_init_ptr: int, episode_length: int):
+        """Closed-loop MPC rollouts (batch.hpp:172-212) from device x_init [B][n_x];
+        totals in REWARD, truncations in ROLLOUT_STATUS."""
+        c = cfg.c()
+        _raise_call(L.lib().docp_rollout(self.h, C.byref(c), x_init_ptr, episode_length))
+
+    def rollout_backward(self, cfg: PcgConfig):
+        """rollout_backward (batch.hpp:221-258) of the last rollout into GRAD_THETA."""
+        c = cfg.c()
+        _raise_call(L.lib().docp_rollout_backward(self.h, C.byref(c)))
+
+    def rollout_errors(self) -> List[Optional[Error]]:
+        st = self.download(L.F_ROLLOUT_STATUS)
+        return [status_error(L.Status(*[int(x) for x in st[j]])) for j in range(self.B)]
 
 
 # --------------------------------------------------------------------------- results

@@ -50,6 +50,10 @@ struct docp_batch {
   std::vector<void*> allocs;
   int max_hist = 0;
   double last_eps_pd = 1e-6;
+  // rollout record (docp_rollout / docp_rollout_backward), grown on demand
+  docp_dev::RolloutRec roll{};
+  int roll_cap = -1;  // episode steps the record holds
+  double roll_eps_pd = 1e-6;
   // profiling: CUDA events around every launch, per kernel kind, on the batch stream
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[DOCP_PROF_KINDS];

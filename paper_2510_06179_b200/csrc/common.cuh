@@ -134,12 +134,25 @@ struct View {
   int max_hist;
 };
 
+/// Rollout record of one batch: every step's solution (for the backward
+/// re-linearisation), the chained states and controls, per-instance flags.
+struct RolloutRec {
+  double *z, *lam;     // [H][B][n_z], [H][B][n_lambda]
+  double *x, *u;       // [H+1][B][n_x], [H][B][n_u]
+  double *xbar, *ex;   // [B][n_x] backward state cotangent, env VJP in x
+  double *gtot;        // [B][n_theta] accumulated gradient
+  double* reward;      // [B]
+  int* alive;          // [B] rollout (and then backward) still running
+  docp_status* rstat;  // [B] first truncation
+  int H;
+};
+
 // ------------------------------------------------------------ status helpers
 __device__ inline void set_status(docp_status* st, int code, int where, int index) {
   st->code = code;
   st->where = where;
   st->index = index;
-  st->reserved = 0;
+  st->step = 0;
 }
 
 // ------------------------------------------------------------ PTX wrappers

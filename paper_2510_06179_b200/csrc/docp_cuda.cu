@@ -19,6 +19,7 @@
 #include "batch.cuh"
 #include "families.cuh"
 #include "k_assemble.cuh"
+#include "k_rollout.cuh"
 #include "k_step.cuh"
 
 using namespace docp_dev;
@@ -303,11 +304,16 @@ double* field_base(docp_batch* b, int f, size_t* per, size_t* elem) {
     case DOCP_F_MU: *per = 1; return b->v.mu;
     case DOCP_F_ALPHA: *per = 1; return b->v.alpha;
     case DOCP_F_LOSS: *per = 1; return b->v.loss;
+    case DOCP_F_REWARD: *per = 1; return b->roll.reward;
     default: break;
   }
   *elem = sizeof(int);
   switch (f) {
     case DOCP_F_STATUS: *per = 1; *elem = sizeof(docp_status); return reinterpret_cast<double*>(b->v.status);
+    case DOCP_F_ROLLOUT_STATUS:
+      *per = 1;
+      *elem = sizeof(docp_status);
+      return reinterpret_cast<double*>(b->roll.rstat);
     case DOCP_F_SQP_ITERS: *per = 1; return reinterpret_cast<double*>(b->v.sqp_iters);
     case DOCP_F_CONVERGED: *per = 1; return reinterpret_cast<double*>(b->v.converged);
     case DOCP_F_PCG_ITERS: *per = 1; return reinterpret_cast<double*>(b->v.pcg_iters);
@@ -403,6 +409,12 @@ int docp_batch_create(const docp_problem* problem, int32_t batch_size, int32_t d
   A(b->list[1], B);
   A(b->counts, 8);
   A(v.pcg_acc, 3);
+  A(b->roll.reward, B);
+  A(b->roll.alive, B);
+  A(b->roll.rstat, B);
+  A(b->roll.xbar, B * d.nx);
+  A(b->roll.ex, B * d.nx);
+  A(b->roll.gtot, B * d.nth);
 #undef A
   if ((rc = ensure_hist(b, 20))) {
     delete b;
@@ -681,6 +693,69 @@ int docp_backward_vjp(docp_batch* b, const docp_pcg_config* cfg) {  // backward.
   return DOCP_OK;
 }
 
+// ---------------------------------------------------------------- rollouts (batch.hpp:172-258)
+namespace {
+int ensure_rollout(docp_batch* b, int H) {
+  if (H <= b->roll_cap) return DOCP_OK;
+  const Dims& d = b->d;
+  const size_t B = static_cast<size_t>(b->B), h = static_cast<size_t>(H);
+  int rc;
+  if ((rc = dalloc(b, &b->roll.z, h * B * d.nz)) || (rc = dalloc(b, &b->roll.lam, h * B * d.nl)) ||
+      (rc = dalloc(b, &b->roll.x, (h + 1) * B * d.nx)) || (rc = dalloc(b, &b->roll.u, h * B * d.nu)))
+    return rc;
+  b->roll_cap = H;
+  return DOCP_OK;
+}
+}  // namespace
+
+int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init, int32_t H) {
+  if (!b || !cfg || !x_init) return fail(DOCP_INVALID, "null argument");
+  if (b->prob.family != DOCP_AFFINE_QUADRATIC)
+    return fail(DOCP_UNSUPPORTED, "rollout: the device environment is the affine family's own dynamics");
+  if (H < 1) return fail(DOCP_DIMENSION, "rollout: episode length must be >= 1");
+  int rc = validate_sqp(cfg);
+  if (rc) return rc;
+  if ((rc = ensure_rollout(b, H))) return rc;
+  b->roll.H = H;
+  b->roll_eps_pd = cfg->eps_pd;
+  const int g = grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8);
+  rollout_init_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, x_init);
+  LAUNCH_CHECK();
+  for (int t = 0; t < H; ++t) {
+    rollout_pre_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t);
+    LAUNCH_CHECK();
+    if ((rc = docp_sqp_solve(b, cfg))) return rc;
+    rollout_post_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t);
+    LAUNCH_CHECK();
+  }
+  return DOCP_OK;
+}
+
+int docp_rollout_backward(docp_batch* b, const docp_pcg_config* cfg) {
+  if (!b || !cfg) return fail(DOCP_INVALID, "null argument");
+  const int H = b->roll.H;
+  if (H < 1 || b->roll_cap < H) return fail(DOCP_INVALID, "rollout_backward: no rollout recorded");
+  const int g = grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8);
+  rollout_back_init_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 256, b->num_sms * 8), 256, 0,
+                             b->stream>>>(b->v, b->roll);
+  LAUNCH_CHECK();
+  int rc;
+  for (int t = H - 1; t >= 0; --t) {
+    CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, sizeof(int), b->stream));
+    rollout_back_pre_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t, b->list[0], b->counts + 1);
+    LAUNCH_CHECK();
+    // the step's cached matrices: re-linearised at its recorded solution
+    if ((rc = launch_assemble(b, b->list[0], b->counts + 1, b->B, b->roll_eps_pd, 1))) return rc;
+    if ((rc = docp_backward_vjp(b, cfg))) return rc;
+    rollout_back_post_kernel<<<grid_for(b->B, 128, b->num_sms * 4), 128, 0, b->stream>>>(b->v, b->roll, t);
+    LAUNCH_CHECK();
+  }
+  rollout_back_fini_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 256, b->num_sms * 8), 256, 0,
+                             b->stream>>>(b->v, b->roll);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
 int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weights, int32_t learn_start,
                   int32_t learn_size, const double* demos, double den, double* loss_sum, double* grad_sum) {
   if (!b || !cfg || !weights || !demos || !loss_sum || !grad_sum) return fail(DOCP_INVALID, "null argument");
@@ -771,6 +846,13 @@ const char* docp_last_error(void) { return g_last_error.c_str(); }
 
 int docp_format_status(const docp_status* s, char* buf, int32_t cap) {
   if (!s || !buf || cap <= 0) return 0;
+  if (s->step > 0) {  // RolloutTruncation wrapping a solve failure (batch.hpp:186-191)
+    docp_status inner = *s;
+    inner.step = 0;
+    const int n = snprintf(buf, cap, "rollout: solve failed at step %d: ", s->step - 1);
+    if (n < 0 || n >= cap) return n;
+    return n + docp_format_status(&inner, buf + n, cap - n);
+  }
   const int i = s->index;
   switch (s->where) {  // messages of common.hpp / problem.hpp / schur.hpp / pcg.hpp / sqp.hpp
     case DOCP_AT_NONE: return snprintf(buf, cap, "ok");
@@ -788,6 +870,8 @@ int docp_format_status(const docp_status* s, char* buf, int32_t cap) {
     case DOCP_AT_MERIT_CONTROL: return snprintf(buf, cap, "merit: non-finite control cost at stage %d", i);
     case DOCP_AT_SQP_ITERATE: return snprintf(buf, cap, "sqp: non-finite iterate at iteration %d", i);
     case DOCP_AT_INITIAL_GUESS: return snprintf(buf, cap, "sqp: initial guess must be finite");
+    case DOCP_AT_ROLLOUT_ENV:
+      return snprintf(buf, cap, "rollout: environment produced a non-finite state at step %d", i);
     default: return snprintf(buf, cap, "error %d at %d", s->code, i);
   }
 }

@@ -346,3 +346,48 @@ def test_error_statuses(D):
         D.sqp_solve(prob, th[0], np.full(nz, np.inf), np.zeros(nl))
     with pytest.raises(D.DimensionError):
         D.sqp_solve(prob, th[0], np.zeros(nz), np.zeros(nl), D.SqpConfig(step_candidates=(1.0, 1.0)))
+
+
+# ----------------------------------------------------------------- rollouts
+
+
+@pytest.mark.skipif(not po.available("ref"), reason="needs the reference build (oracle/_ref)")
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+@pytest.mark.parametrize("one_step", [True, False])
+def test_rollout_affine_matches_reference(D, mode, one_step):
+    """rollout + rollout_backward (batch.hpp:172-258) with the affine
+    environment (train.hpp:195-213) against the reference's own functions:
+    total rewards and d(reward)/dtheta bit-identical in PARITY, 1e-9 in FAST;
+    a NaN-weighted instance is truncated with the reference's message."""
+    import torch
+    nx, nu, T, B, H = 4, 2, 20, 6, 5
+    th = po.gen_aq(nx, nu, T, 5, B, convex=False)   # random_linear_instance (make_linear_rl_task)
+    th[4, 0] = np.nan                                 # solve fails at step 0
+    x0 = th[:, -nx:].copy()                           # x_inits = inst.x_s
+    if one_step:  # the benchmark's real-time mode (train.hpp:226-230)
+        ocfg = po.sqp_config(max_sqp_iters=1, alphas=(1.0,))
+        gcfg = D.SqpConfig(max_sqp_iters=1, step_candidates=[1.0], pcg=D.PcgConfig(mode=mode))
+    else:
+        ocfg = po.sqp_config()
+        gcfg = D.SqpConfig(pcg=D.PcgConfig(mode=mode))
+    want_r, want_g, ok, msgs = po.rollout_affine(nx, nu, T, th, x0, H, ocfg)
+    assert not ok[4] and ok.sum() == B - 1
+    b = D.Batch(D.affine_quadratic(nx, nu, T), B)
+    b.upload(D._lib.F_THETA, th)
+    xi = torch.tensor(x0, device="cuda")
+    b.rollout(gcfg, xi.data_ptr(), H)
+    b.rollout_backward(gcfg.pcg)
+    got_r = b.download(D._lib.F_REWARD)[:, 0]
+    got_g = b.download(D._lib.F_GRAD_THETA)
+    errs = b.rollout_errors()
+    for j in range(B):
+        if not ok[j]:
+            assert isinstance(errs[j], D.RolloutTruncation) and str(errs[j]) == msgs[j], (str(errs[j]), msgs[j])
+            continue
+        assert errs[j] is None
+        if mode == "parity":
+            assert got_r[j] == want_r[j], (j, got_r[j], want_r[j])
+            assert np.array_equal(got_g[j], want_g[j]), (j, np.abs(got_g[j] - want_g[j]).max())
+        else:
+            assert abs(got_r[j] - want_r[j]) <= RTOL_FAST * max(1.0, abs(want_r[j]))
+            assert rel(got_g[j], want_g[j]) <= RTOL_FAST
