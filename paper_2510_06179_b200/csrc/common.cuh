@@ -51,6 +51,8 @@ __host__ __device__ inline int uoff(const Dims& d, int t) { return t * (d.nx + d
 ///            (chunks 2h, 2h+1 of every column) or column halves)
 ///   NX = 4: s' = s ^ (b & 3),   chunk' = chunk ^ ((b >> 2) & 1)
 ///           (pcg_kernel: one thread per block row)
+///   NX = 16: chunk' = chunk ^ (b & 1)
+///           (pcg_kernel_h16f: four threads per block row, rows 4q..4q+3)
 ///   other : plain column-major.
 __host__ __device__ inline int blk_off(int nx, int b, int e, int s) {
   if (nx == 8) {
@@ -62,6 +64,7 @@ __host__ __device__ inline int blk_off(int nx, int b, int e, int s) {
     const int sp = s ^ (b & 3);
     return sp * 4 + ((((e >> 1) ^ ((b >> 2) & 1)) << 1) | (e & 1));
   }
+  if (nx == 16) return s * 16 + ((((e >> 1) ^ (b & 1)) << 1) | (e & 1));
   return s * nx + e;
 }
 
@@ -79,6 +82,11 @@ __host__ __device__ inline void blk_entry(int nx, int b, int o, int* e, int* s) 
     *e = ((((o >> 1) & 1) ^ ((b >> 2) & 1)) << 1) | (o & 1);
     return;
   }
+  if (nx == 16) {
+    *s = o >> 4;
+    *e = ((((o >> 1) & 7) ^ (b & 1)) << 1) | (o & 1);
+    return;
+  }
   *s = o / nx;
   *e = o % nx;
 }
@@ -88,6 +96,7 @@ __host__ __device__ inline void blk_entry(int nx, int b, int o, int* e, int* s) 
 __host__ __device__ inline int vec_off(int nx, int j, int e) {
   if (nx == 8) return j * 8 + ((((e >> 1) ^ ((j >> 1) & 3)) << 1) | (e & 1));
   if (nx == 4) return j * 4 + ((((e >> 1) ^ ((j >> 2) & 1)) << 1) | (e & 1));
+  if (nx == 16) return j * 16 + ((((e >> 1) ^ (j & 1)) << 1) | (e & 1));
   return j * nx + e;
 }
 

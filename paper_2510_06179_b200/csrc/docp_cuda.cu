@@ -153,6 +153,7 @@ int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint
   if (nx == 8 && nu == 2) return launch_assemble_t<8, 2>(b, list, count, n_hint, eps_pd, do_schur);
   if (nx == 4 && nu == 2) return launch_assemble_t<4, 2>(b, list, count, n_hint, eps_pd, do_schur);
   if (nx == 4 && nu == 1) return launch_assemble_t<4, 1>(b, list, count, n_hint, eps_pd, do_schur);
+  if (nx == 16 && nu == 8) return launch_assemble_t<16, 8>(b, list, count, n_hint, eps_pd, do_schur);
   const int sp = std::max(b->d.bsz, b->d.nx * b->d.nu);
   const size_t smem = static_cast<size_t>(kAsmWarps) * 6 * sp * sizeof(double);
   CUDA_TRY(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -209,6 +210,7 @@ int launch_pcg(docp_batch* b, const docp_pcg_config& cfg, const int* list, const
   switch (b->d.nx) {
     case 4: return launch_pcg_nx4(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
     case 8: return launch_pcg_nx8(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+    case 16: return launch_pcg_nx16(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
     default: return launch_pcg_nxrt(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
   }
 }
@@ -883,10 +885,11 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const bool res = pcg_smem(d, true) + 64 <= static_cast<size_t>(max_optin);
-  const int cl = h8f_cluster_for(d, dev);
+  const int cl = d.nx == 16 ? h16f_cluster_for(d, dev) : h8f_cluster_for(d, dev);
+  const char* fk = d.nx == 16 ? "pcg_kernel_h16f" : "pcg_kernel_h8f";
   char fast[64];
-  if (cl == 1) snprintf(fast, sizeof fast, "pcg_kernel_h8f(resident)");
-  else if (cl > 1) snprintf(fast, sizeof fast, "pcg_kernel_h8f(cluster%d,resident)", cl);
+  if (cl == 1) snprintf(fast, sizeof fast, "%s(resident)", fk);
+  else if (cl > 1) snprintf(fast, sizeof fast, "%s(cluster%d,resident)", fk, cl);
   else snprintf(fast, sizeof fast, "%s", d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
                                                    : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>");
   const char* parity = d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")

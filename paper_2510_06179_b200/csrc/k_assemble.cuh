@@ -385,7 +385,7 @@ struct AsmLayout {
 };
 
 template <int NX, int NU>
-__global__ void __launch_bounds__(kAsmGroupThreads, 4) assemble_kernel_t(View v, const int* __restrict__ work,
+__global__ void __launch_bounds__(kAsmGroupThreads, NX >= 16 ? 2 : 4) assemble_kernel_t(View v, const int* __restrict__ work,
                                                                       const int* __restrict__ n_work, double eps_pd,
                                                                       int do_schur) {
   static_assert(32 % NX == 0, "group size must divide the warp");

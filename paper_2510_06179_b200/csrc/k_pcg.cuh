@@ -58,8 +58,8 @@ __device__ __forceinline__ void load_col(const double* region, int b, int s, int
     }
   } else {
     const int n = NX > 0 ? NX : nx;
-    const double* base = region + static_cast<long>(b) * n * n + s * n;
-    for (int e = 0; e < n; ++e) out[e] = ld1<SMEM>(base + e);
+    const double* base = region + static_cast<long>(b) * n * n;
+    for (int e = 0; e < n; ++e) out[e] = ld1<SMEM>(base + blk_off(n, b, e, s));
   }
 }
 
