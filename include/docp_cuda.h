@@ -222,10 +222,12 @@ int docp_il_epoch(docp_batch* batch, const docp_sqp_config* cfg, const double* w
  * (make_affine_env, train.hpp:195-213). For each instance: the initial-state
  * segment of THETA is set to the current state, the problem is solved warm-
  * started from the previous step (Z, LAMBDA; zero at step 0), the first
- * control is applied, the reward accumulated. x_init: device [B][n_x].
+ * control is applied, the reward accumulated. x_init: [B][n_x], on the device
+ * when x_init_on_device != 0, else host memory (copied synchronously).
  * Per-instance truncations go to ROLLOUT_STATUS; REWARD receives the totals.
  * Every step's solution is recorded on the device for docp_rollout_backward. */
-int docp_rollout(docp_batch* batch, const docp_sqp_config* cfg, const double* x_init, int32_t episode_length);
+int docp_rollout(docp_batch* batch, const docp_sqp_config* cfg, const double* x_init, int32_t x_init_on_device,
+                 int32_t episode_length);
 /* rollout_backward (batch.hpp:221-258) of the last rollout: GRAD_THETA <-
  * dJ/dtheta of the total reward, its initial-state segment = dJ/dx_init.
  * The adjoint multiplier is chained across steps; instances whose rollout

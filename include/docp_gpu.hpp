@@ -14,6 +14,8 @@
 //   pcg_solve(sys, gamma, lambda0, cfg)          pcg_solve(sys, gamma, lambda0, cfg)                pcg.hpp:52-109
 //   batch_solve(instances, cache, cfg, workers)  batch_solve(family, instances, cache, cfg)          batch.hpp:83-108
 //   (train_il inner loop, train.hpp:82-109)      BatchSolver::solve + BatchSolver::backward
+//   rollout / rollout_backward (batch.hpp:172-258, affine env train.hpp:195-213)
+//                                                BatchSolver::rollout + BatchSolver::rollout_backward
 //
 // Behaviour kept from the reference:
 //   * argument checks with the reference's DimensionError messages;
@@ -389,9 +391,67 @@ class BatchSolver {
     return out;
   }
 
+  /// docp::rollout (batch.hpp:172-212) of every instance with its own affine
+  /// dynamics as the environment and reward -(|x'|^2 + |u|^2) (make_affine_env,
+  /// train.hpp:195-213). Returns the total rewards; errors[j] receives the
+  /// reference's RolloutTruncation text for a truncated instance.
+  std::vector<double> rollout(const std::vector<const ParameterVector*>& thetas, const std::vector<Vector>& x_init,
+                              int episode_length, const SqpConfig& cfg, std::vector<std::string>* errors = nullptr) {
+    cfg.validate();
+    const int B = size(), nth = b_->n_theta(), nx = b_->problem().n_x;
+    require(static_cast<int>(thetas.size()) == B && static_cast<int>(x_init.size()) == B,
+            "batch: instance count does not match the batch size");
+    require(episode_length >= 1, "rollout: episode length must be >= 1");
+    std::vector<double> th(static_cast<std::size_t>(B) * nth), x0(static_cast<std::size_t>(B) * nx);
+    for (int j = 0; j < B; ++j) {
+      require(x_init[j].size() == nx, "rollout: initial state length mismatch");
+      require(thetas[j]->size() == nth, "docp_gpu: theta length does not match the family layout");
+      detail::put(th, static_cast<std::size_t>(j) * nth, thetas[j]->values());
+      detail::put(x0, static_cast<std::size_t>(j) * nx, x_init[j]);
+    }
+    b_->upload(DOCP_F_THETA, th);
+    const docp_sqp_config c = detail::to_c(cfg, opt_.mode);
+    {
+      detail::CountPcg count;
+      detail::check(docp_rollout(b_->get(), &c, x0.data(), 0, episode_length));
+    }
+    auto reward = b_->download<double>(DOCP_F_REWARD);
+    roll_status(errors);
+    return reward;
+  }
+
+  /// docp::rollout_backward (batch.hpp:221-258) of the last rollout:
+  /// d(total reward)/d theta per instance, the initial-state segment holding
+  /// d/dx_init. Truncated instances get an empty vector.
+  std::vector<Vector> rollout_backward(const PcgConfig& cfg, std::vector<std::string>* errors = nullptr) {
+    const docp_pcg_config c = detail::to_c(cfg, opt_.mode);
+    {
+      detail::CountPcg count;
+      detail::check(docp_rollout_backward(b_->get(), &c));
+    }
+    const int nth = b_->n_theta();
+    auto g = b_->download<double>(DOCP_F_GRAD_THETA);
+    auto st = roll_status(errors);
+    std::vector<Vector> out(size());
+    for (int j = 0; j < size(); ++j)
+      if (st[j].code == DOCP_OK) out[j] = detail::to_vec(&g[static_cast<std::size_t>(j) * nth], nth);
+    return out;
+  }
+
   const std::vector<docp_status>& last_status() const { return last_status_; }
 
  private:
+  std::vector<docp_status> roll_status(std::vector<std::string>* errors) {
+    auto st = b_->download<docp_status>(DOCP_F_ROLLOUT_STATUS);
+    if (errors) {
+      errors->assign(size(), std::string());
+      for (int j = 0; j < size(); ++j)
+        if (st[j].code != DOCP_OK) (*errors)[j] = detail::status_message(st[j]);
+    }
+    last_status_ = st;
+    return st;
+  }
+
   Options opt_;
   std::shared_ptr<detail::Batch> b_;
   std::vector<docp_status> last_status_;

@@ -84,7 +84,7 @@ SIGNATURES = {
     "docp_sqp_solve": (C.c_int, [_vp, C.POINTER(SqpConfigC)]),
     "docp_backward_vjp": (C.c_int, [_vp, C.POINTER(PcgConfigC)]),
     "docp_il_epoch": (C.c_int, [_vp, C.POINTER(SqpConfigC), _vp, _i32, _i32, _vp, _dbl, _vp, _vp]),
-    "docp_rollout": (C.c_int, [_vp, C.POINTER(SqpConfigC), _vp, _i32]),
+    "docp_rollout": (C.c_int, [_vp, C.POINTER(SqpConfigC), _vp, _i32, _i32]),
     "docp_rollout_backward": (C.c_int, [_vp, C.POINTER(PcgConfigC)]),
     "docp_generate_affine_quadratic": (C.c_int, [_i32, _i32, _u64, _i32, _i32, _dp]),
     "docp_generate_uniform": (C.c_int, [_u64, _i32, _dbl, _dbl, _dp]),

@@ -362,11 +362,18 @@ class Batch:
                                           loss_denominator, loss_sum_ptr, grad_sum_ptr))
 
 
-    def rollout(self, cfg: SqpConfig, x_init_ptr: int, episode_length: int):
-        """Closed-loop MPC rollouts (batch.hpp:172-212) from device x_init [B][n_x];
-        totals in REWARD, truncations in ROLLOUT_STATUS."""
+    def rollout(self, cfg: SqpConfig, x_init, episode_length: int):
+        """Closed-loop MPC rollouts (batch.hpp:172-212) from x_init [B][n_x]
+        (a device pointer as int, or a host array); totals in REWARD,
+        truncations in ROLLOUT_STATUS."""
         c = cfg.c()
-        _raise_call(L.lib().docp_rollout(self.h, C.byref(c), x_init_ptr, episode_length))
+        if isinstance(x_init, int):
+            _raise_call(L.lib().docp_rollout(self.h, C.byref(c), x_init, 1, episode_length))
+        else:
+            arr = np.ascontiguousarray(x_init, dtype=np.float64)
+            if arr.size != self.B * self.problem.n_x:
+                raise DimensionError("rollout: initial state length mismatch")
+            _raise_call(L.lib().docp_rollout(self.h, C.byref(c), arr.ctypes.data, 0, episode_length))
 
     def rollout_backward(self, cfg: PcgConfig):
         """rollout_backward (batch.hpp:221-258) of the last rollout into GRAD_THETA."""

@@ -710,7 +710,8 @@ int ensure_rollout(docp_batch* b, int H) {
 }
 }  // namespace
 
-int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init, int32_t H) {
+int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init, int32_t x_init_on_device,
+                 int32_t H) {
   if (!b || !cfg || !x_init) return fail(DOCP_INVALID, "null argument");
   if (b->prob.family != DOCP_AFFINE_QUADRATIC)
     return fail(DOCP_UNSUPPORTED, "rollout: the device environment is the affine family's own dynamics");
@@ -720,6 +721,10 @@ int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init
   if ((rc = ensure_rollout(b, H))) return rc;
   b->roll.H = H;
   b->roll_eps_pd = cfg->eps_pd;
+  if (!x_init_on_device) {  // stage the host states in the record's x_0 slot
+    CUDA_TRY(cudaMemcpyAsync(b->roll.x, x_init, sizeof(double) * b->B * b->d.nx, cudaMemcpyHostToDevice, b->stream));
+    x_init = b->roll.x;
+  }
   const int g = grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8);
   rollout_init_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, x_init);
   LAUNCH_CHECK();

@@ -14,6 +14,7 @@
 #include <random>
 
 #include "docp/bench/generators.hpp"
+#include "docp/bench/train.hpp"
 #include "docp_gpu.hpp"
 
 using namespace docp;
@@ -342,5 +343,36 @@ TEST_CASE("gpu BatchSolver: train_il inner loop (solve, loss, backward) matches 
     BackwardResult bc = backward_vjp(cpu, grads[i], lts[i], ocp, thetas[i], cfg.pcg);
     CHECK(same(back[i].grad_theta, bc.grad_theta));
     CHECK(back[i].pcg_iters == bc.pcg_iters);
+  }
+}
+
+TEST_CASE("gpu BatchSolver: rollout + rollout_backward match the reference (affine env)") {  // batch.hpp:172-258
+  const int n = 5, T = 20, H = 4;
+  std::mt19937_64 rng(11);
+  std::vector<AffineQuadratic> probs;
+  std::vector<ParameterVector> thetas;
+  std::vector<const ParameterVector*> tp;
+  std::vector<Vector> x0;
+  for (int i = 0; i < n; ++i) {
+    probs.push_back(bench::random_linear_instance(4, 2, T, rng));
+    thetas.push_back(probs.back().make_theta());
+    x0.push_back(probs.back().x_s);
+  }
+  for (auto& t : thetas) tp.push_back(&t);
+  SqpConfig cfg;
+  cfg.max_sqp_iters = 1;
+  cfg.step_candidates = {1.0};  // make_linear_rl_task's real-time mode (train.hpp:226-230)
+  gpu::BatchSolver solver(gpu::family_of(probs[0]), n, parity());
+  std::vector<std::string> errs;
+  auto rewards = solver.rollout(tp, x0, H, cfg, &errs);
+  auto grads = solver.rollout_backward(cfg.pcg, &errs);
+  for (int i = 0; i < n; ++i) {
+    OcpDefinition ocp = probs[i].make_ocp();
+    DiffEnv env = bench::make_affine_env(probs[i]);
+    RolloutOutput roll = rollout(env, ocp, thetas[i], x0[i], H, cfg);
+    Vector g = rollout_backward(roll.record, env, ocp, thetas[i], cfg.pcg);
+    CHECK(errs[i].empty());
+    CHECK(rewards[i] == roll.total_reward);
+    CHECK(same(grads[i], g));
   }
 }

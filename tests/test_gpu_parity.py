@@ -375,7 +375,7 @@ def test_rollout_affine_matches_reference(D, mode, one_step):
     b = D.Batch(D.affine_quadratic(nx, nu, T), B)
     b.upload(D._lib.F_THETA, th)
     xi = torch.tensor(x0, device="cuda")
-    b.rollout(gcfg, xi.data_ptr(), H)
+    b.rollout(gcfg, xi.data_ptr() if one_step else x0, H)  # device and host x_init paths
     b.rollout_backward(gcfg.pcg)
     got_r = b.download(D._lib.F_REWARD)[:, 0]
     got_g = b.download(D._lib.F_GRAD_THETA)
