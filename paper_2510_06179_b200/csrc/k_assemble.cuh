@@ -384,15 +384,17 @@ struct AsmLayout {
   static constexpr int GBUF = RAW + ((SKEW - RAW % 16) % 16 + 16) % 16;
 };
 
-template <int NX, int NU>
-__global__ void __launch_bounds__(kAsmGroupThreads, NX >= 16 ? 2 : 4) assemble_kernel_t(View v, const int* __restrict__ work,
+/// TH threads per CTA (TH / NX stage groups); the launcher picks TH so that the
+/// groups divide the horizon's stages into whole rounds where it can.
+template <int NX, int NU, int TH>
+__global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assemble_kernel_t(View v, const int* __restrict__ work,
                                                                       const int* __restrict__ n_work, double eps_pd,
                                                                       int do_schur) {
   static_assert(32 % NX == 0, "group size must divide the warp");
   using Lay = AsmLayout<NX, NU>;
   constexpr int B2 = NX * NX;
   constexpr int LD = Lay::LD, LDU = Lay::LDU;
-  constexpr int NG = kAsmGroupThreads / NX;
+  constexpr int NG = TH / NX;
   extern __shared__ double sm_asm[];
   __shared__ AsmShared sh;
   const Dims d = v.d;
