@@ -30,7 +30,8 @@
  * with the reference's message (docp_format_status).
  *
  * Layouts (fp64, per problem, problems contiguous):
- *   THETA   family layout (affine_quadratic.hpp:27-37, cartpole.hpp:82-89)
+ *   THETA   family layout (affine_quadratic.hpp:27-37, cartpole.hpp:82-89,
+ *           attitude.hpp:44-53 + the instance inertia, see DOCP_ATTITUDE)
  *   Z       flat interleaved (x_0,u_0,...,x_{T-1},u_{T-1},x_T)  trajectory.hpp:7-39
  *   LAMBDA  n_x*(T+1)
  * Schur blocks move through docp_batch_{upload,download}_schur in the
@@ -54,7 +55,11 @@ extern "C" {
 
 #define DOCP_ABI_VERSION 1
 
-enum docp_family { DOCP_AFFINE_QUADRATIC = 1, DOCP_CARTPOLE = 2 };
+/* DOCP_ATTITUDE (attitude.hpp): n_x = n_u = 3, cost scale 0.5, dt from
+ * docp_problem.dt. Its per-instance AttitudeParams::inertia rides in THETA's
+ * tail: THETA = [w_x 3 | w_u 3 | omega_0 3 | inertia 3] (the reference's 9
+ * entries, make_attitude_theta, then the inertia); GRAD_THETA's inertia tail is 0. */
+enum docp_family { DOCP_AFFINE_QUADRATIC = 1, DOCP_CARTPOLE = 2, DOCP_ATTITUDE = 3 };
 
 /* docp::Error hierarchy (common.hpp:18-54) plus ABI-level failures. */
 enum docp_code {
@@ -101,7 +106,7 @@ typedef struct docp_problem {
   int32_t n_x, n_u, horizon;
   double cost_scale;                             /* affine-quadratic (affine_quadratic.hpp:25) */
   double cart_mass, pole_mass, length, gravity;  /* cart-pole (cartpole.hpp:17-26) */
-  double dt;
+  double dt;                                     /* cart-pole and attitude time step */
 } docp_problem;
 
 /* PCG arithmetic: PARITY reproduces the reference's operation order
@@ -217,9 +222,11 @@ int docp_il_epoch(docp_batch* batch, const docp_sqp_config* cfg, const double* w
                   int32_t learn_size, const double* demos, double loss_denominator, double* loss_sum,
                   double* grad_sum);
 
-/* Closed-loop MPC rollouts (batch.hpp:172-212) of affine-quadratic instances
- * with their own dynamics as the environment and reward -(|x'|^2 + |u|^2)
- * (make_affine_env, train.hpp:195-213). For each instance: the initial-state
+/* Closed-loop MPC rollouts (batch.hpp:172-212) with the benchmark tasks'
+ * environments: affine-quadratic instances step their own dynamics with
+ * reward -(|x'|^2 + |u|^2) (make_affine_env, train.hpp:195-213); attitude
+ * instances step attitude_step with reward -(0.1 |x'|^2 + |u|^2)
+ * (make_attitude_rl_task, train.hpp:239-263). For each instance: the initial-state
  * segment of THETA is set to the current state, the problem is solved warm-
  * started from the previous step (Z, LAMBDA; zero at step 0), the first
  * control is applied, the reward accumulated. x_init: [B][n_x], on the device

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-enum { PORT_AFFINE_QUADRATIC = 1, PORT_CARTPOLE = 2 };
+enum { PORT_AFFINE_QUADRATIC = 1, PORT_CARTPOLE = 2, PORT_ATTITUDE = 3 /* ref build only */ };
 enum {
   PORT_OK = 0,
   PORT_DIMENSION = 1,
@@ -35,7 +35,8 @@ typedef struct {
   int family;
   int nx, nu, horizon;
   double cost_scale;                                   /* affine-quadratic */
-  double cart_mass, pole_mass, length, gravity, dt;    /* cart-pole */
+  double cart_mass, pole_mass, length, gravity, dt;    /* cart-pole (dt: attitude too) */
+  double inertia[3];                                   /* attitude (AttitudeParams, attitude.hpp:10-14) */
 } port_problem;
 
 typedef struct {

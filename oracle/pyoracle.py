@@ -23,7 +23,7 @@ LIBS = {
     "ref": os.path.join(HERE, "_ref", "libdocp_ref.so"),
 }
 
-AFFINE_QUADRATIC, CARTPOLE = 1, 2
+AFFINE_QUADRATIC, CARTPOLE, ATTITUDE = 1, 2, 3
 CODES = {0: "OK", 1: "DIMENSION", 2: "EVALUATION", 3: "NUMERICAL", 4: "BREAKDOWN", 5: "DIVERGENCE", 99: "ERROR"}
 
 
@@ -32,6 +32,7 @@ class Problem(C.Structure):
         ("family", C.c_int), ("nx", C.c_int), ("nu", C.c_int), ("horizon", C.c_int),
         ("cost_scale", C.c_double), ("cart_mass", C.c_double), ("pole_mass", C.c_double),
         ("length", C.c_double), ("gravity", C.c_double), ("dt", C.c_double),
+        ("inertia", C.c_double * 3),
     ]
 
 
@@ -72,9 +73,17 @@ def cartpole_problem(T=40, cart_mass=1.0, pole_mass=0.1, length=0.5, gravity=9.8
     return Problem(CARTPOLE, 4, 1, T, 0.5, cart_mass, pole_mass, length, gravity, dt)
 
 
+def attitude_problem(T=25, inertia=(1.0, 1.0, 1.0), dt=0.1) -> Problem:
+    """AttitudeParams (attitude.hpp:10-14); ref build only."""
+    p = Problem(ATTITUDE, 3, 3, T, 0.5, 0.0, 0.0, 0.0, 0.0, dt)
+    for k in range(3):
+        p.inertia[k] = inertia[k]
+    return p
+
+
 def theta_size(p: Problem) -> int:
-    if p.family == CARTPOLE:
-        return 9
+    if p.family in (CARTPOLE, ATTITUDE):
+        return 2 * p.nx + p.nu
     return p.nx + p.nu + p.nx * p.nx + p.nx * p.nu + 2 * p.nx
 
 
@@ -154,6 +163,9 @@ def load(kind: str):
             lib.ref_spectral_radius.restype = C.c_double
             lib.ref_spectral_radius.argtypes = [dp, C.c_int]
             lib.ref_pcg_invocations.restype = C.c_ulonglong
+            lib.ref_rollout_attitude.restype = C.c_int
+            lib.ref_rollout_attitude.argtypes = [C.c_int, C.c_double, C.c_int, dp, dp, dp, C.c_int,
+                                                 C.POINTER(SqpConfig), dp, dp, ip, C.c_char_p]
             lib.ref_rollout_affine.restype = C.c_int
             lib.ref_rollout_affine.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int,
                                                C.POINTER(SqpConfig), dp, dp, ip, C.c_char_p]
@@ -359,6 +371,20 @@ def rollout_affine(nx, nu, T, thetas, x_inits, episode_length, cfg):
     raw = msgs.raw
     messages = [raw[256 * j:256 * (j + 1)].split(b"\0")[0].decode() for j in range(B)]
     return rewards, grads, ok.astype(bool), messages
+
+
+def rollout_attitude(T, dt, thetas, inertias, x_inits, episode_length, cfg):
+    """The reference's rollout + rollout_backward with the attitude RL environment
+    (train.hpp:239-263), per instance (ref only): (rewards, grads[9], ok, messages)."""
+    lib = load("ref")
+    B = thetas.shape[0]
+    rewards, grads = np.zeros(B), np.zeros((B, 9))
+    ok = np.zeros(B, np.int32)
+    msgs = C.create_string_buffer(256 * B)
+    lib.ref_rollout_attitude(T, dt, B, _p(_arr(thetas)), _p(_arr(inertias)), _p(_arr(x_inits)), episode_length,
+                             C.byref(cfg), _p(rewards), _p(grads), ok.ctypes.data_as(C.POINTER(C.c_int)), msgs)
+    raw = msgs.raw
+    return rewards, grads, ok.astype(bool), [raw[256 * j:256 * (j + 1)].split(b"\0")[0].decode() for j in range(B)]
 
 
 def gen_cartpole(seed, horizon, n_demos):

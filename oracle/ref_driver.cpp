@@ -59,6 +59,13 @@ void put(const Matrix& m, double* out) {
 /// Family -> OcpDefinition. AffineQuadratic reads every coefficient from
 /// theta (affine_quadratic.hpp:39-81), so the struct only carries sizes.
 OcpDefinition make_ocp(const port_problem& p) {
+  if (p.family == PORT_ATTITUDE) {
+    AttitudeParams ap;
+    ap.inertia = vec(p.inertia, 3);
+    ap.dt = p.dt;
+    ap.horizon = p.horizon;
+    return make_attitude_ocp(ap);
+  }
   if (p.family == PORT_CARTPOLE) {
     CartpoleParams cp;
     cp.cart_mass = p.cart_mass;
@@ -85,10 +92,10 @@ ParameterVector make_theta(const port_problem& p, const double* th) {
     theta.add_segment(name, vec(th + k, n));
     k += n;
   };
-  if (p.family == PORT_CARTPOLE) {
-    seg(segment::state_cost, 4);
-    seg(segment::control_cost, 1);
-    seg(segment::initial_state, 4);
+  if (p.family == PORT_CARTPOLE || p.family == PORT_ATTITUDE) {
+    seg(segment::state_cost, p.nx);
+    seg(segment::control_cost, p.nu);
+    seg(segment::initial_state, p.nx);
   } else {
     seg(segment::state_cost, p.nx);
     seg(segment::control_cost, p.nu);
@@ -362,7 +369,9 @@ int ref_il_epoch(const port_problem* p, int batch, const double* thetas, const d
   clear(st);
   OcpDefinition ocp = make_ocp(*p);
   SqpConfig cfg = make_cfg(*c);
-  const int nth = p->family == PORT_CARTPOLE ? 9 : p->nx + p->nu + p->nx * p->nx + p->nx * p->nu + 2 * p->nx;
+  const int nth = (p->family == PORT_CARTPOLE || p->family == PORT_ATTITUDE)
+                      ? 2 * p->nx + p->nu
+                      : p->nx + p->nu + p->nx * p->nx + p->nx * p->nu + 2 * p->nx;
   const Eigen::Index nz = ocp.primal_size(), nl = ocp.dual_size();
   std::vector<std::string> errors(static_cast<std::size_t>(batch));
   std::vector<Vector> g(static_cast<std::size_t>(batch));
@@ -472,6 +481,40 @@ int ref_rollout_affine(int nx, int nu, int horizon, int batch, const double* the
       Vector g = rollout_backward(roll.record, env, ocp, theta, cfg.pcg);
       rewards[j] = roll.total_reward;
       put(g, grads + j * nth);
+      ok[j] = 1;
+    } catch (const Error& e) {
+      ok[j] = 0;
+      std::snprintf(messages + j * 256, 256, "%s", e.what());
+    }
+  });
+  return 0;
+}
+
+/// rollout + rollout_backward of attitude instances with the attitude RL
+/// task's environment (make_attitude_rl_task, train.hpp:239-263): step =
+/// attitude_step, reward -(0.1 |x|^2 + |u|^2). thetas: [batch][9] (reference
+/// layout), inertias: [batch][3].
+int ref_rollout_attitude(int horizon, double dt, int batch, const double* thetas, const double* inertias,
+                         const double* x_inits, int episode_length, const port_sqp_config* c, double* rewards,
+                         double* grads, int* ok, char* messages) {
+  SqpConfig cfg = make_cfg(*c);
+  parallel_for(static_cast<std::size_t>(batch), 0, [&](std::size_t j) {
+    AttitudeParams p;
+    p.inertia = vec(inertias + 3 * j, 3);
+    p.dt = dt;
+    p.horizon = horizon;
+    OcpDefinition ocp = make_attitude_ocp(p);
+    ParameterVector theta = make_attitude_theta(vec(thetas + 9 * j, 3), vec(thetas + 9 * j + 3, 3),
+                                                vec(thetas + 9 * j + 6, 3));
+    DiffEnv env = make_diff_env(
+        [p](const Vector& x, const Vector& u) { return attitude_step(p, x, u); },
+        [](const Vector& x, const Vector& u) { return -(0.1 * x.squaredNorm() + u.squaredNorm()); },
+        [](const Vector& x, const Vector& u) { return std::make_pair(Vector(-0.2 * x), Vector(-2.0 * u)); });
+    try {
+      RolloutOutput roll = rollout(env, ocp, theta, vec(x_inits + 3 * j, 3), episode_length, cfg);
+      Vector g = rollout_backward(roll.record, env, ocp, theta, cfg.pcg);
+      rewards[j] = roll.total_reward;
+      put(g, grads + 9 * j);
       ok[j] = 1;
     } catch (const Error& e) {
       ok[j] = 0;

@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libdocp_cuda.so")
 
-AFFINE_QUADRATIC, CARTPOLE = 1, 2
+AFFINE_QUADRATIC, CARTPOLE, ATTITUDE = 1, 2, 3
 OK, DIMENSION, EVALUATION, NUMERICAL, BREAKDOWN, DIVERGENCE, UNSUPPORTED, CUDA_ERROR, INVALID = range(9)
 PCG_FAST, PCG_PARITY = 0, 1
 RHS_FORWARD, RHS_ADJOINT = 0, 1

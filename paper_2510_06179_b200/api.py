@@ -162,6 +162,13 @@ def cartpole(horizon: int = 40, cart_mass: float = 1.0, pole_mass: float = 0.1, 
     return L.Problem(L.CARTPOLE, 4, 1, horizon, 0.5, cart_mass, pole_mass, length, gravity, dt)
 
 
+def attitude(horizon: int = 25, dt: float = 0.1) -> L.Problem:
+    """Attitude-rate family (attitude.hpp:10-72). Device theta =
+    [w_x(3) | w_u(3) | omega_0(3) | inertia(3)]: make_attitude_theta's 9
+    entries, then the instance's AttitudeParams::inertia (d theta of it is 0)."""
+    return L.Problem(L.ATTITUDE, 3, 3, horizon, 0.5, 0.0, 0.0, 0.0, 0.0, dt)
+
+
 def theta_size(problem: L.Problem) -> int:
     return L.lib().docp_theta_size(C.byref(problem))
 

@@ -337,13 +337,15 @@ double* field_base(docp_batch* b, int f, size_t* per, size_t* elem) {
 
 int check_problem(const docp_problem* p) {
   if (!p) return fail(DOCP_INVALID, "null problem");
-  if (p->family != DOCP_AFFINE_QUADRATIC && p->family != DOCP_CARTPOLE)
+  if (p->family != DOCP_AFFINE_QUADRATIC && p->family != DOCP_CARTPOLE && p->family != DOCP_ATTITUDE)
     return fail(DOCP_UNSUPPORTED, "unknown problem family %d", p->family);
   if (p->n_x < 1 || p->n_u < 1 || p->horizon < 1) return fail(DOCP_DIMENSION, "dimensions must be positive");
   if (p->n_x > kMaxNx || p->n_u > kMaxNu)
     return fail(DOCP_UNSUPPORTED, "n_x, n_u must be <= %d (got %d, %d)", kMaxNx, p->n_x, p->n_u);
   if (p->family == DOCP_CARTPOLE && (p->n_x != 4 || p->n_u != 1))
     return fail(DOCP_DIMENSION, "cart-pole has n_x = 4, n_u = 1");
+  if (p->family == DOCP_ATTITUDE && (p->n_x != 3 || p->n_u != 3))
+    return fail(DOCP_DIMENSION, "attitude has n_x = n_u = 3");
   return DOCP_OK;
 }
 
@@ -721,8 +723,8 @@ int ensure_rollout(docp_batch* b, int H) {
 int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init, int32_t x_init_on_device,
                  int32_t H) {
   if (!b || !cfg || !x_init) return fail(DOCP_INVALID, "null argument");
-  if (b->prob.family != DOCP_AFFINE_QUADRATIC)
-    return fail(DOCP_UNSUPPORTED, "rollout: the device environment is the affine family's own dynamics");
+  if (b->prob.family == DOCP_CARTPOLE)
+    return fail(DOCP_UNSUPPORTED, "rollout: environments exist for the affine and attitude tasks");
   if (H < 1) return fail(DOCP_DIMENSION, "rollout: episode length must be >= 1");
   int rc = validate_sqp(cfg);
   if (rc) return rc;

@@ -34,7 +34,7 @@ struct Family {
   __host__ __device__ static Family from(const docp_problem& p) {
     Family f;
     f.kind = p.family;
-    f.scale = p.family == DOCP_CARTPOLE ? 0.5 : p.cost_scale;
+    f.scale = p.family == DOCP_AFFINE_QUADRATIC ? p.cost_scale : 0.5;  // quadratic_cost scale 0.5
     f.cart_mass = p.cart_mass;
     f.pole_mass = p.pole_mass;
     f.length = p.length;
@@ -47,7 +47,7 @@ struct Family {
   __device__ const double* w_u(const Dims& d, const double* th) const { return th + d.nx; }
   /// initial_state(theta)
   __device__ const double* x_s(const Dims& d, const double* th) const {
-    if (kind == DOCP_CARTPOLE) return th + 5;
+    if (kind != DOCP_AFFINE_QUADRATIC) return th + d.nx + d.nu;  // [w_x | w_u | x_0 (| ...)]
     return th + d.nx + d.nu + d.nx * d.nx + d.nx * d.nu + d.nx;
   }
 
@@ -76,6 +76,36 @@ struct Family {
         for (int k = 0; k < nx * nx; ++k) jx[k] = -a[k];
       if (ju)
         for (int k = 0; k < nx * nu; ++k) ju[k] = -b[k];
+      return;
+    }
+    if (kind == DOCP_ATTITUDE) {  // make_explicit_dynamics(attitude_step), attitude.hpp:16-42
+      const double* in = th + 9;   // AttitudeParams::inertia (THETA tail)
+      double jw[3], h[3], ji[3], xn_[3];
+      for (int i = 0; i < 3; ++i) jw[i] = in[i] * x[i];
+      h[0] = jw[1] * x[2] - jw[2] * x[1];  // jw.cross(w)
+      h[1] = jw[2] * x[0] - jw[0] * x[2];
+      h[2] = jw[0] * x[1] - jw[1] * x[0];
+      for (int i = 0; i < 3; ++i) ji[i] = 1.0 / in[i];
+      for (int i = 0; i < 3; ++i) xn_[i] = x[i] + dt * (ji[i] * (h[i] + u[i]));
+      for (int i = 0; i < 3; ++i) res[i] = xn[i] - xn_[i];
+      if (jx) {  // jac_x = I + (dt j_inv) .* (skew(jw) - skew(w) diag(J)), negated
+        double sj[9], sw[9];  // row-major skew matrices (attitude.hpp:16-20)
+        auto skew = [](const double* v, double* m) {
+          m[0] = 0.0, m[1] = -v[2], m[2] = v[1];
+          m[3] = v[2], m[4] = 0.0, m[5] = -v[0];
+          m[6] = -v[1], m[7] = v[0], m[8] = 0.0;
+        };
+        skew(jw, sj);
+        skew(x, sw);
+        for (int i = 0; i < 3; ++i)
+          for (int k = 0; k < 3; ++k) {
+            const double dh = sj[3 * i + k] - sw[3 * i + k] * in[k];
+            jx[i + 3 * k] = -((i == k ? 1.0 : 0.0) + (dt * ji[i]) * dh);
+          }
+      }
+      if (ju)
+        for (int i = 0; i < 3; ++i)
+          for (int k = 0; k < 3; ++k) ju[i + 3 * k] = -(dt * (i == k ? ji[i] : 0.0));
       return;
     }
     // cart-pole: make_explicit_dynamics(cartpole_step), cartpole.hpp:28-78

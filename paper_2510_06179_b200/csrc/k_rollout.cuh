@@ -1,7 +1,10 @@
 // k_rollout.cuh — closed-loop MPC rollouts on the device:
 // the per-step glue of docp::rollout / rollout_backward (batch.hpp:172-258)
-// for the affine-quadratic family with its own dynamics as the environment
-// and reward R(x', u) = -(|x'|^2 + |u|^2) (make_affine_env, train.hpp:195-213).
+// with the benchmark tasks' environments: each instance steps its own
+// dynamics x' = phi(x, u) (explicit step of the family; the affine family's
+// x' = A x + B u + b) with reward R(x', u) = -(w_r |x'|^2 + |u|^2), w_r = 1
+// for the affine task (make_affine_env, train.hpp:195-213) and 0.1 for the
+// attitude task (make_attitude_rl_task, train.hpp:239-263).
 // The solves themselves are the batched K1-K4 path; these kernels only move
 // states between steps, apply the environment, and chain the cotangents. One
 // warp per instance; lane 0 does the n_x-sized arithmetic in the reference's
@@ -12,7 +15,20 @@
 
 namespace docp_dev {
 
-__device__ inline int xs_off(const Dims& d) { return d.nx + d.nu + d.nx * d.nx + d.nx * d.nu + d.nx; }
+__device__ inline int xs_off(const Dims& d, const Family& fam) {
+  return fam.kind == DOCP_AFFINE_QUADRATIC ? d.nx + d.nu + d.nx * d.nx + d.nx * d.nu + d.nx : d.nx + d.nu;
+}
+/// Reward weight on |x'|^2 of the family's RL task.
+__device__ inline double reward_wx(const Family& fam) { return fam.kind == DOCP_ATTITUDE ? 0.1 : 1.0; }
+/// x' = phi(x, u): the explicit step, as -f(x' = 0, x, u) (exact: the
+/// residual is 0 - phi, every family's phi(x,u) is evaluated as in its step).
+__device__ inline void env_step(const Dims& d, const Family& fam, const double* th, const double* x, const double* u,
+                                double* xn) {
+  double zero[kMaxNx], res[kMaxNx];
+  for (int i = 0; i < d.nx; ++i) zero[i] = 0.0;
+  fam.dynamics(d, th, zero, x, u, res, nullptr, nullptr);
+  for (int i = 0; i < d.nx; ++i) xn[i] = -res[i];
+}
 
 /// Step 0: x_0 = x_init, zero warm starts, everything alive.
 __global__ void rollout_init_kernel(View v, RolloutRec rr, const double* __restrict__ x_init) {
@@ -39,7 +55,7 @@ __global__ void rollout_pre_kernel(View v, RolloutRec rr, int t) {
   const Dims d = v.d;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  const int xs = xs_off(d);
+  const int xs = xs_off(d, Family::from(v.prob));
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < v.B; p += warps) {
     const double* xt = rr.x + (static_cast<long>(t) * v.B + p) * d.nx;
     if (rr.alive[p]) {
@@ -73,23 +89,17 @@ __global__ void rollout_post_kernel(View v, RolloutRec rr, int t) {
     double* xn = rr.x + (static_cast<long>(t + 1) * v.B + p) * nx;
     double* u = rr.u + (static_cast<long>(t) * v.B + p) * nu;
     if (lane == 0) {
+      const Family fam = Family::from(v.prob);
       const double* th = v.theta + static_cast<long>(p) * d.nth;
-      const double* a = th + nx + nu;
-      const double* b = a + nx * nx;
-      const double* off = b + nx * nu;
-      double uu[kMaxNu];
+      double uu[kMaxNu], xv[kMaxNx];
       for (int i = 0; i < nu; ++i) uu[i] = z[uoff(d, 0) + i];  // policy_first_control (sqp.hpp:264-266)
+      env_step(d, fam, th, x, uu, xv);
       bool fin = true;
       double sx = 0.0;
-      for (int i = 0; i < nx; ++i) {  // x' = A x + B u + b
-        double ax = a[i] * x[0];
-        for (int k = 1; k < nx; ++k) ax = ax + a[i + k * nx] * x[k];
-        double bu = b[i] * uu[0];
-        for (int k = 1; k < nu; ++k) bu = bu + b[i + k * nx] * uu[k];
-        const double val = (ax + bu) + off[i];
-        xn[i] = val;
-        fin = fin && isfinite(val);
-        sx = i == 0 ? val * val : sx + val * val;
+      for (int i = 0; i < nx; ++i) {
+        xn[i] = xv[i];
+        fin = fin && isfinite(xv[i]);
+        sx = i == 0 ? xv[i] * xv[i] : sx + xv[i] * xv[i];
       }
       double su = uu[0] * uu[0];
       for (int i = 1; i < nu; ++i) su = su + uu[i] * uu[i];
@@ -98,7 +108,7 @@ __global__ void rollout_post_kernel(View v, RolloutRec rr, int t) {
         set_status(rr.rstat + p, DOCP_DIVERGENCE, DOCP_AT_ROLLOUT_ENV, t);
         rr.alive[p] = 0;
       } else {
-        rr.reward[p] = rr.reward[p] + (-(sx + su));
+        rr.reward[p] = rr.reward[p] + (-(reward_wx(fam) * sx + su));
       }
     }
     // record the step's solution (warm_z / warm_lambda stay in Z, LAMBDA)
@@ -120,7 +130,8 @@ __global__ void rollout_back_pre_kernel(View v, RolloutRec rr, int t, int* __res
   const int nx = d.nx, nu = d.nu;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  const int xs = xs_off(d);
+  const Family fam = Family::from(v.prob);
+  const int xs = xs_off(d, fam);
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < v.B; p += warps) {
     if (!rr.alive[p]) {
       if (lane == 0) set_status(v.status + p, DOCP_DIVERGENCE, DOCP_AT_ROLLOUT_ENV, -1);
@@ -139,20 +150,22 @@ __global__ void rollout_back_pre_kernel(View v, RolloutRec rr, int t, int* __res
     for (int e = lane; e < d.nl; e += 32) v.lam[static_cast<long>(p) * d.nl + e] = rl[e];
     __syncwarp();
     if (lane == 0) {
-      const double* a = th + nx + nu;
-      const double* b = a + nx * nx;
+      // step_vjp: the step's Jacobians (dphi/dx, dphi/du) = -(jac_x, jac_u) of the residual
+      double jx[kMaxNx * kMaxNx], ju[kMaxNx * kMaxNu], res[kMaxNx];
+      fam.dynamics(d, th, xn, x, u, res, jx, ju);
       double* xbar = rr.xbar + static_cast<long>(p) * nx;
       double* ex = rr.ex + static_cast<long>(p) * nx;
+      const double rx = fam.kind == DOCP_ATTITUDE ? -0.2 : -2.0;  // reward_grad (train.hpp:208-211, 254-257)
       double cot[kMaxNx];
-      for (int i = 0; i < nx; ++i) cot[i] = xbar[i] + (-2.0 * xn[i]);  // xbar + r_x
-      for (int k = 0; k < nx; ++k) {  // e_x = A' cot
-        double s = a[k * nx] * cot[0];
-        for (int i = 1; i < nx; ++i) s = s + a[i + k * nx] * cot[i];
+      for (int i = 0; i < nx; ++i) cot[i] = xbar[i] + (rx * xn[i]);  // xbar + r_x
+      for (int k = 0; k < nx; ++k) {  // e_x = jac_x' cot
+        double s = (-jx[k * nx]) * cot[0];
+        for (int i = 1; i < nx; ++i) s = s + (-jx[i + k * nx]) * cot[i];
         ex[k] = s;
       }
-      for (int k = 0; k < nu; ++k) {  // ubar = r_u + B' cot
-        double s = b[k * nx] * cot[0];
-        for (int i = 1; i < nx; ++i) s = s + b[i + k * nx] * cot[i];
+      for (int k = 0; k < nu; ++k) {  // ubar = r_u + jac_u' cot
+        double s = (-ju[k * nx]) * cot[0];
+        for (int i = 1; i < nx; ++i) s = s + (-ju[i + k * nx]) * cot[i];
         lg[uoff(d, 0) + k] = (-2.0 * u[k]) + s;
       }
       list[atomicAdd(count, 1)] = p;
@@ -166,7 +179,7 @@ __global__ void rollout_back_pre_kernel(View v, RolloutRec rr, int t, int* __res
 __global__ void rollout_back_post_kernel(View v, RolloutRec rr, int t) {
   const Dims d = v.d;
   const int nx = d.nx;
-  const int xs = xs_off(d);
+  const int xs = xs_off(d, Family::from(v.prob));
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < v.B; p += gridDim.x * blockDim.x) {
     if (!rr.alive[p]) continue;
     const docp_status st = v.status[p];
@@ -203,7 +216,7 @@ __global__ void rollout_back_init_kernel(View v, RolloutRec rr) {
 
 __global__ void rollout_back_fini_kernel(View v, RolloutRec rr) {
   const Dims d = v.d;
-  const int xs = xs_off(d);
+  const int xs = xs_off(d, Family::from(v.prob));
   for (long g = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; g < static_cast<long>(v.B) * d.nth;
        g += static_cast<long>(gridDim.x) * blockDim.x) {
     const int p = static_cast<int>(g / d.nth), k = static_cast<int>(g % d.nth);

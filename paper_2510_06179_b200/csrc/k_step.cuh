@@ -364,8 +364,8 @@ __global__ void vjp_kernel(View v, const int* __restrict__ work, const int* __re
     } else if (k < nx + nu) {
       const int i = k - nx;
       for (int t = 0; t < T; ++t) acc = acc - s2 * (z[uoff(d, t) + i] * zt[uoff(d, t) + i]);
-    } else if (fam.kind == DOCP_CARTPOLE) {  // initial state
-      acc = acc + lt[k - 5];
+    } else if (fam.kind != DOCP_AFFINE_QUADRATIC) {  // initial state (quadratic_cost.hpp:24-45)
+      if (k < 2 * nx + nu) acc = acc + lt[k - nx - nu];  // attitude's inertia tail: 0
     } else {
       const int e = k - nx - nu;
       if (e < nx * nx) {  // dA(i,j) += lam_{t+1,i} z~x_{t,j} + lam~_{t+1,i} x_{t,j}

@@ -391,3 +391,71 @@ def test_rollout_affine_matches_reference(D, mode, one_step):
         else:
             assert abs(got_r[j] - want_r[j]) <= RTOL_FAST * max(1.0, abs(want_r[j]))
             assert rel(got_g[j], want_g[j]) <= RTOL_FAST
+
+
+# ----------------------------------------------------------------- attitude family
+
+
+def _attitude_set(B, seed):
+    rng = np.random.default_rng(seed)
+    inertia = rng.uniform(0.5, 2.0, (B, 3))
+    w0 = rng.uniform(-1.0, 1.0, (B, 3))
+    th9 = np.concatenate([np.ones((B, 3)), np.ones((B, 3)), w0], axis=1)  # make_attitude_theta, Q = R = I
+    return th9, inertia
+
+
+@pytest.mark.skipif(not po.available("ref"), reason="needs the reference build (oracle/_ref)")
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_sqp_backward_attitude(D, mode):
+    """Attitude-rate family (attitude.hpp) against the reference: SQP from
+    z = 0 (4 iterations, make_attitude_rl_task) and the backward pass."""
+    B, T = 5, 25
+    th9, inertia = _attitude_set(B, 3)
+    prob = D.attitude(T, 0.1)
+    nz, nl = D.sizes(prob)
+    th = np.concatenate([th9, inertia], axis=1)
+    cfg = D.SqpConfig(max_sqp_iters=4, pcg=D.PcgConfig(mode=mode))
+    res, errs = D.sqp_solve_batch(prob, th, np.zeros((B, nz)), np.zeros((B, nl)), cfg)
+    assert all(e is None for e in errs)
+    lg = np.random.default_rng(4).standard_normal((B, nz))
+    grads, lts, its, errs = D.backward_vjp_batch(res[0].batch, lg, np.zeros((B, nl)), cfg.pcg)
+    assert all(e is None for e in errs)
+    for j in range(B):
+        o = po.Oracle("ref", po.attitude_problem(T, inertia[j], 0.1))
+        s = o.sqp_solve(th9[j], np.zeros(nz), np.zeros(nl), po.sqp_config(max_sqp_iters=4))
+        g, lt, it = o.backward(th9[j], lg[j], np.zeros(nl))
+        assert res[j].sqp_iters == s.sqp_iters and res[j].pcg_iters == s.pcg_iters and its[j] == it
+        assert np.all(grads[j][9:] == 0.0)
+        if mode == "parity":
+            assert np.array_equal(res[j].z, s.z) and np.array_equal(res[j].lam, s.lam)
+            assert np.array_equal(grads[j][:9], g) and np.array_equal(lts[j], lt)
+            assert res[j].kkt_inf_norm == s.kkt and res[j].step_sizes == s.step_sizes
+        else:
+            for got, want in ((res[j].z, s.z), (res[j].lam, s.lam), (grads[j][:9], g), (lts[j], lt)):
+                assert rel(got, want) <= RTOL_FAST
+
+
+@pytest.mark.skipif(not po.available("ref"), reason="needs the reference build (oracle/_ref)")
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_rollout_attitude_matches_reference(D, mode):
+    """rollout + rollout_backward with the attitude RL environment
+    (make_attitude_rl_task, train.hpp:239-263) against the reference."""
+    B, T, H = 5, 25, 4
+    th9, inertia = _attitude_set(B, 8)
+    x0 = th9[:, 6:9].copy()
+    want_r, want_g, ok, msgs = po.rollout_attitude(T, 0.1, th9, inertia, x0, H, po.sqp_config(max_sqp_iters=4))
+    assert ok.all(), msgs
+    b = D.Batch(D.attitude(T, 0.1), B)
+    b.upload(D._lib.F_THETA, np.concatenate([th9, inertia], axis=1))
+    cfg = D.SqpConfig(max_sqp_iters=4, pcg=D.PcgConfig(mode=mode))
+    b.rollout(cfg, x0, H)
+    b.rollout_backward(cfg.pcg)
+    assert all(e is None for e in b.rollout_errors())
+    got_r = b.download(D._lib.F_REWARD)[:, 0]
+    got_g = b.download(D._lib.F_GRAD_THETA)[:, :9]
+    for j in range(B):
+        if mode == "parity":
+            assert got_r[j] == want_r[j] and np.array_equal(got_g[j], want_g[j]), (j, got_r[j], want_r[j])
+        else:
+            assert abs(got_r[j] - want_r[j]) <= RTOL_FAST * abs(want_r[j])
+            assert rel(got_g[j], want_g[j]) <= RTOL_FAST
