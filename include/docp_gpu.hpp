@@ -42,6 +42,7 @@
 #include "docp/backward.hpp"
 #include "docp/batch.hpp"
 #include "docp/problems/affine_quadratic.hpp"
+#include "docp/problems/attitude.hpp"
 #include "docp/problems/cartpole.hpp"
 #include "docp/sqp.hpp"
 #include "docp_cuda.h"
@@ -51,6 +52,9 @@ namespace docp::gpu {
 /// What the device needs instead of OcpDefinition's callbacks.
 struct Family {
   docp_problem desc{};
+  /// Per-problem constants the device keeps after theta's reference layout
+  /// (attitude: AttitudeParams::inertia); appended to thetas that omit them.
+  std::vector<double> theta_tail;
 };
 
 /// AffineQuadratic::make_ocp (affine_quadratic.hpp:39-81).
@@ -61,6 +65,19 @@ inline Family family_of(const AffineQuadratic& p) {
   f.desc.n_u = p.n_u;
   f.desc.horizon = p.horizon;
   f.desc.cost_scale = p.cost_scale;
+  return f;
+}
+
+/// make_attitude_ocp (attitude.hpp:55-72); the inertia rides in theta's tail.
+inline Family family_of(const AttitudeParams& p) {
+  Family f;
+  f.desc.family = DOCP_ATTITUDE;
+  f.desc.n_x = 3;
+  f.desc.n_u = 3;
+  f.desc.horizon = p.horizon;
+  f.desc.cost_scale = 0.5;
+  f.desc.dt = p.dt;
+  for (Eigen::Index i = 0; i < p.inertia.size(); ++i) f.theta_tail.push_back(p.inertia[i]);
   return f;
 }
 
@@ -204,6 +221,18 @@ inline void put(std::vector<double>& dst, std::size_t off, const Vector& v) {
   for (Eigen::Index i = 0; i < v.size(); ++i) dst[off + static_cast<std::size_t>(i)] = v[i];
 }
 
+/// theta in the device layout: the reference values, then the family's tail
+/// when the caller passed the reference layout alone.
+inline void put_theta(std::vector<double>& dst, std::size_t off, const ParameterVector& theta, int nth,
+                      const std::vector<double>& tail) {
+  const Eigen::Index n = theta.size();
+  require(n == nth || n + static_cast<Eigen::Index>(tail.size()) == nth,
+          "docp_gpu: theta length does not match the family layout");
+  put(dst, off, theta.values());
+  if (n < nth)
+    for (std::size_t k = 0; k < tail.size(); ++k) dst[off + static_cast<std::size_t>(n) + k] = tail[k];
+}
+
 /// QpData and SchurSystem of every problem, from the device (the matrices
 /// the forward pass left resident for the backward pass).
 inline void materialize(Batch& b, std::vector<SolveResult*>& out) {
@@ -270,7 +299,7 @@ inline void materialize(Batch& b, std::vector<SolveResult*>& out) {
 class BatchSolver {
  public:
   BatchSolver(const Family& family, int batch_size, Options opt = {})
-      : opt_(opt), b_(std::make_shared<detail::Batch>(family.desc, batch_size, opt)) {}
+      : opt_(opt), tail_(family.theta_tail), b_(std::make_shared<detail::Batch>(family.desc, batch_size, opt)) {}
 
   int size() const { return b_->size(); }
   detail::Batch& batch() { return *b_; }
@@ -297,8 +326,7 @@ class BatchSolver {
                 "trajectory dimensions do not match the problem");  // problem.hpp:62-65
         require(lambda0[j].size() == nl, "sqp: dual guess length mismatch");
         require(z0[j].all_finite() && lambda0[j].allFinite(), "sqp: initial guess must be finite");
-        require(thetas[j]->size() == nth, "docp_gpu: theta length does not match the family layout");
-        detail::put(th, static_cast<std::size_t>(j) * nth, thetas[j]->values());
+        detail::put_theta(th, static_cast<std::size_t>(j) * nth, *thetas[j], nth, tail_);
         detail::put(z, static_cast<std::size_t>(j) * nz, z0[j].flatten());
         detail::put(l, static_cast<std::size_t>(j) * nl, lambda0[j]);
       } catch (const Error& e) {
@@ -383,7 +411,8 @@ class BatchSolver {
         if (errors) (*errors)[j] = detail::status_message(st[j]);
         continue;
       }
-      out[j].grad_theta = detail::to_vec(&gt[static_cast<std::size_t>(j) * nth], nth);
+      out[j].grad_theta =
+          detail::to_vec(&gt[static_cast<std::size_t>(j) * nth], nth - static_cast<Eigen::Index>(tail_.size()));
       out[j].lambda_tilde = detail::to_vec(&lts[static_cast<std::size_t>(j) * nl], nl);
       out[j].pcg_iters = its[j];
     }
@@ -405,8 +434,7 @@ class BatchSolver {
     std::vector<double> th(static_cast<std::size_t>(B) * nth), x0(static_cast<std::size_t>(B) * nx);
     for (int j = 0; j < B; ++j) {
       require(x_init[j].size() == nx, "rollout: initial state length mismatch");
-      require(thetas[j]->size() == nth, "docp_gpu: theta length does not match the family layout");
-      detail::put(th, static_cast<std::size_t>(j) * nth, thetas[j]->values());
+      detail::put_theta(th, static_cast<std::size_t>(j) * nth, *thetas[j], nth, tail_);
       detail::put(x0, static_cast<std::size_t>(j) * nx, x_init[j]);
     }
     b_->upload(DOCP_F_THETA, th);
@@ -434,7 +462,8 @@ class BatchSolver {
     auto st = roll_status(errors);
     std::vector<Vector> out(size());
     for (int j = 0; j < size(); ++j)
-      if (st[j].code == DOCP_OK) out[j] = detail::to_vec(&g[static_cast<std::size_t>(j) * nth], nth);
+      if (st[j].code == DOCP_OK)
+        out[j] = detail::to_vec(&g[static_cast<std::size_t>(j) * nth], nth - static_cast<Eigen::Index>(tail_.size()));
     return out;
   }
 
@@ -453,6 +482,7 @@ class BatchSolver {
   }
 
   Options opt_;
+  std::vector<double> tail_;
   std::shared_ptr<detail::Batch> b_;
   std::vector<docp_status> last_status_;
 };
@@ -483,9 +513,8 @@ inline BackwardResult backward_vjp(const SolveResult& result, const Vector& loss
   require(lambda_tilde0.size() == result.qp.dual_size(), "backward_vjp: warm start length mismatch");
   ocp.check_dims(result.z);
   detail::Batch b(family.desc, 1, opt);
-  require(theta.size() == b.n_theta(), "docp_gpu: theta length does not match the family layout");
   std::vector<double> th(b.n_theta()), z(b.n_z()), l(b.n_lambda()), g(b.n_z()), lt(b.n_lambda());
-  detail::put(th, 0, theta.values());
+  detail::put_theta(th, 0, theta, b.n_theta(), family.theta_tail);
   detail::put(z, 0, result.z.flatten());
   detail::put(l, 0, result.lambda);
   detail::put(g, 0, loss_grad_z);
@@ -507,7 +536,8 @@ inline BackwardResult backward_vjp(const SolveResult& result, const Vector& loss
   st = b.download<docp_status>(DOCP_F_STATUS);
   if (st[0].code != DOCP_OK) detail::throw_status(st[0]);
   BackwardResult out;
-  out.grad_theta = detail::to_vec(b.download<double>(DOCP_F_GRAD_THETA).data(), b.n_theta());
+  out.grad_theta = detail::to_vec(b.download<double>(DOCP_F_GRAD_THETA).data(),
+                                  b.n_theta() - static_cast<Eigen::Index>(family.theta_tail.size()));
   out.lambda_tilde = detail::to_vec(b.download<double>(DOCP_F_LAMBDA_TILDE).data(), b.n_lambda());
   out.pcg_iters = b.download<int32_t>(DOCP_F_PCG_ITERS)[0];
   return out;

@@ -376,3 +376,39 @@ TEST_CASE("gpu BatchSolver: rollout + rollout_backward match the reference (affi
     CHECK(same(grads[i], g));
   }
 }
+
+TEST_CASE("gpu attitude family: sqp_solve, backward_vjp and rollouts match the reference") {  // attitude.hpp
+  AttitudeParams params;
+  params.inertia = (Vector(3) << 1.5, 0.7, 1.1).finished();
+  params.horizon = 25;
+  OcpDefinition ocp = make_attitude_ocp(params);
+  ParameterVector theta =
+      make_attitude_theta(Vector::Ones(3), Vector::Ones(3), (Vector(3) << 0.4, -0.8, 0.3).finished());
+  SqpConfig cfg;
+  cfg.max_sqp_iters = 4;  // make_attitude_rl_task (train.hpp:258-261)
+  Trajectory z0(3, 3, 25);
+  SolveResult cpu = sqp_solve(ocp, theta, z0, Vector::Zero(ocp.dual_size()), cfg);
+  SolveResult dev = gpu::sqp_solve(gpu::family_of(params), ocp, theta, z0, Vector::Zero(ocp.dual_size()), cfg,
+                                   parity());
+  CHECK(same(dev.z.flatten(), cpu.z.flatten()));
+  CHECK(dev.pcg_iters == cpu.pcg_iters);
+  Vector g = loss_grad(cpu.z, 5);
+  BackwardResult bc = backward_vjp(cpu, g, Vector::Zero(ocp.dual_size()), ocp, theta, cfg.pcg);
+  BackwardResult bd =
+      gpu::backward_vjp(dev, g, Vector::Zero(ocp.dual_size()), gpu::family_of(params), ocp, theta, cfg.pcg, parity());
+  CHECK(same(bd.grad_theta, bc.grad_theta));
+  // rollouts with the attitude RL environment (train.hpp:239-263)
+  DiffEnv env = make_diff_env([params](const Vector& x, const Vector& u) { return attitude_step(params, x, u); },
+                              [](const Vector& x, const Vector& u) { return -(0.1 * x.squaredNorm() + u.squaredNorm()); },
+                              [](const Vector& x, const Vector& u) {
+                                return std::make_pair(Vector(-0.2 * x), Vector(-2.0 * u));
+                              });
+  Vector x0 = theta.segment(segment::initial_state);
+  RolloutOutput roll = rollout(env, ocp, theta, x0, 3, cfg);
+  Vector gr = rollout_backward(roll.record, env, ocp, theta, cfg.pcg);
+  gpu::BatchSolver solver(gpu::family_of(params), 1, parity());
+  auto rewards = solver.rollout({&theta}, {x0}, 3, cfg);
+  auto grads = solver.rollout_backward(cfg.pcg);
+  CHECK(rewards[0] == roll.total_reward);
+  CHECK(same(grads[0], gr));
+}

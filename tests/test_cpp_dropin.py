@@ -19,4 +19,4 @@ def test_cpp_dropin_suite():
     failed = [line for line in r.stdout.splitlines() if line.startswith("FAIL ")]
     passed = [line for line in r.stdout.splitlines() if line.startswith("PASS ")]
     assert r.returncode == 0 and not failed, r.stdout[-4000:] + r.stderr[-2000:]
-    assert len(passed) >= 10
+    assert len(passed) >= 11
