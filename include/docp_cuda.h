@@ -247,6 +247,11 @@ int docp_rollout_backward(docp_batch* batch, const docp_pcg_config* cfg);
 int docp_generate_affine_quadratic(int32_t n_x, int32_t n_u, uint64_t seed, int32_t count, int32_t convex,
                                    double* thetas);
 int docp_generate_uniform(uint64_t seed, int32_t n, double lo, double hi, double* out);
+/* pcg_study's drifting sequence (study.hpp:37-48, 74-124): random_convex_instance
+ * from mt19937_64(seed), coefficients of A, B, b, x_s scaled by 1 + U(-m, m)
+ * after every step; thetas [steps][n_theta]. */
+int docp_generate_drift_sequence(int32_t n_x, int32_t n_u, uint64_t seed, int32_t steps, double magnitude,
+                                 double* thetas);
 /* gen_cartpole initial states (generators.hpp:142-152), [n][4]. */
 int docp_generate_cartpole_x0(uint64_t seed, int32_t n, double* x0);
 

@@ -163,6 +163,8 @@ def load(kind: str):
             lib.ref_spectral_radius.restype = C.c_double
             lib.ref_spectral_radius.argtypes = [dp, C.c_int]
             lib.ref_pcg_invocations.restype = C.c_ulonglong
+            lib.ref_pcg_study.restype = C.c_int
+            lib.ref_pcg_study.argtypes = [dp, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, ip, ip]
             lib.ref_rollout_attitude.restype = C.c_int
             lib.ref_rollout_attitude.argtypes = [C.c_int, C.c_double, C.c_int, dp, dp, dp, C.c_int,
                                                  C.POINTER(SqpConfig), dp, dp, ip, C.c_char_p]
@@ -385,6 +387,18 @@ def rollout_attitude(T, dt, thetas, inertias, x_inits, episode_length, cfg):
                              C.byref(cfg), _p(rewards), _p(grads), ok.ctypes.data_as(C.POINTER(C.c_int)), msgs)
     raw = msgs.raw
     return rewards, grads, ok.astype(bool), [raw[256 * j:256 * (j + 1)].split(b"\0")[0].decode() for j in range(B)]
+
+
+def pcg_study(tols, steps, seed=0, nx=8, nu=4, T=30):
+    """The reference's pcg_study iteration counts: arrays [tol][step][pass] of
+    (cold, warm) with pass 0 = forward, 1 = backward (ref only)."""
+    lib = load("ref")
+    n = len(tols) * steps * 2
+    cold, warm = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    ip_ = C.POINTER(C.c_int)
+    lib.ref_pcg_study(_p(_arr(np.asarray(tols, np.float64))), len(tols), steps, seed, nx, nu, T,
+                      cold.ctypes.data_as(ip_), warm.ctypes.data_as(ip_))
+    return cold.reshape(len(tols), steps, 2), warm.reshape(len(tols), steps, 2)
 
 
 def gen_cartpole(seed, horizon, n_demos):

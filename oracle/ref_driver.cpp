@@ -8,6 +8,7 @@
 // the reference itself, and it exposes the reference's own generators and
 // training loop for golden-vector generation. Nothing here re-implements the
 // algorithm: every numeric result comes from a reference function.
+#include "docp/bench/study.hpp"
 #include "docp/bench/train.hpp"
 #include "docp/oracle.hpp"
 
@@ -522,6 +523,19 @@ int ref_rollout_attitude(int horizon, double dt, int batch, const double* thetas
     }
   });
   return 0;
+}
+
+/// The reference's own pcg_study (study.hpp:56-145): per (tol, step, pass)
+/// cold and warm PCG iteration counts, rows in the report's order
+/// (tol-major, then step, forward before backward). Returns the row count.
+int ref_pcg_study(const double* tols, int n_tols, int steps, std::uint64_t seed, int nx, int nu, int horizon,
+                  int* cold_iters, int* warm_iters) {
+  auto rep = bench::pcg_study(std::vector<double>(tols, tols + n_tols), steps, seed, nx, nu, horizon);
+  for (std::size_t k = 0; k < rep.rows.size(); ++k) {
+    cold_iters[k] = rep.rows[k].cold_iters;
+    warm_iters[k] = rep.rows[k].warm_iters;
+  }
+  return static_cast<int>(rep.rows.size());
 }
 
 /// bench::gen_cartpole (generators.hpp:134-168): initial states (n x 4) and

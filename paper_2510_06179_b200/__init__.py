@@ -7,7 +7,7 @@ from .api import (  # noqa: F401
     EvaluationError, NumericalError, PcgConfig, RolloutTruncation, SolveResult, SqpConfig, WarmStartCache,
     affine_quadratic, attitude,
     backward_vjp, backward_vjp_batch, batch_solve, cartpole, describe, flat_offset, generate_affine_quadratic,
-    generate_cartpole_x0, generate_uniform, kernel_launches,
+    generate_cartpole_x0, generate_drift_sequence, generate_uniform, kernel_launches,
     one_shot_config, pcg_invocations, sizes, sqp_solve, sqp_solve_batch, theta_size,
 )
 from . import _lib  # noqa: F401

@@ -88,6 +88,7 @@ SIGNATURES = {
     "docp_rollout_backward": (C.c_int, [_vp, C.POINTER(PcgConfigC)]),
     "docp_generate_affine_quadratic": (C.c_int, [_i32, _i32, _u64, _i32, _i32, _dp]),
     "docp_generate_uniform": (C.c_int, [_u64, _i32, _dbl, _dbl, _dp]),
+    "docp_generate_drift_sequence": (C.c_int, [_i32, _i32, _u64, _i32, _dbl, _dp]),
     "docp_generate_cartpole_x0": (C.c_int, [_u64, _i32, _dp]),
     "docp_profile_begin": (C.c_int, [_vp]),
     "docp_profile_end": (C.c_int, [_vp, C.POINTER(Profile)]),

@@ -211,6 +211,14 @@ def generate_affine_quadratic(n_x: int, n_u: int, seed: int, count: int, convex:
     return out
 
 
+def generate_drift_sequence(n_x: int, n_u: int, seed: int, steps: int, magnitude: float = 0.01) -> np.ndarray:
+    """pcg_study's slowly drifting instance sequence (study.hpp:37-48, 74-124), [steps][n_theta]."""
+    out = np.zeros((steps, n_x + n_u + n_x * n_x + n_x * n_u + 2 * n_x))
+    _raise_call(L.lib().docp_generate_drift_sequence(n_x, n_u, seed, steps, magnitude,
+                                                     out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
 def generate_uniform(seed: int, n: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
     out = np.zeros(n)
     _raise_call(L.lib().docp_generate_uniform(seed, n, lo, hi, out.ctypes.data_as(C.POINTER(C.c_double))))

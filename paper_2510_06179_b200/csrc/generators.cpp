@@ -218,6 +218,33 @@ int docp_generate_affine_quadratic(int32_t nx, int32_t nu, uint64_t seed, int32_
   return DOCP_OK;
 }
 
+/// The drifting instance sequence of pcg_study (study.hpp:74-77, 123-124 and
+/// perturb_coefficients, study.hpp:37-48): random_convex_instance from
+/// mt19937_64(seed), then after every step each coefficient of A, B, b and
+/// x_s (in that order, column-major) is scaled by 1 + U(-magnitude, magnitude)
+/// drawn from the same engine. thetas: [steps][n_theta].
+int docp_generate_drift_sequence(int32_t nx, int32_t nu, uint64_t seed, int32_t steps, double magnitude,
+                                 double* thetas) {
+  if (nx < 1 || nu < 1 || steps < 0 || !thetas) return DOCP_INVALID;
+  std::mt19937_64 rng(seed);
+  const size_t nth = static_cast<size_t>(nx + nu + nx * nx + nx * nu + 2 * nx);
+  std::vector<double> cur(nth);
+  {
+    std::uniform_real_distribution<double> weight(0.5, 2.0);
+    std::normal_distribution<double> normal(0.0, 1.0);
+    linear_instance(nx, nu, rng, cur.data());
+    for (int i = 0; i < nx; ++i) cur[i] = weight(rng);
+    for (int i = 0; i < nu; ++i) cur[nx + i] = weight(rng);
+    for (int i = 0; i < nx; ++i) cur[nth - nx + i] = normal(rng);
+  }
+  for (int k = 0; k < steps; ++k) {
+    std::copy(cur.begin(), cur.end(), thetas + nth * static_cast<size_t>(k));
+    std::uniform_real_distribution<double> u(-magnitude, magnitude);
+    for (size_t e = static_cast<size_t>(nx + nu); e < nth; ++e) cur[e] *= 1.0 + u(rng);  // A, B, b, x_s
+  }
+  return DOCP_OK;
+}
+
 /// n draws of uniform_real_distribution(lo, hi) from mt19937_64(seed)
 /// (train.hpp:61-64 initial weights; generators.hpp:142-151 initial states).
 int docp_generate_uniform(uint64_t seed, int32_t n, double lo, double hi, double* out) {

@@ -459,3 +459,17 @@ def test_rollout_attitude_matches_reference(D, mode):
         else:
             assert abs(got_r[j] - want_r[j]) <= RTOL_FAST * abs(want_r[j])
             assert rel(got_g[j], want_g[j]) <= RTOL_FAST
+
+
+# ----------------------------------------------------------------- pcg_study
+
+
+@pytest.mark.skipif(not po.available("ref"), reason="needs the reference build (oracle/_ref)")
+def test_pcg_study_matches_reference(D):
+    """The GPU warm-vs-cold study reproduces the reference's pcg_study
+    iteration counts (study.hpp:56-145) for every tol, step and pass."""
+    from paper_2510_06179_b200.study import pcg_study
+    tols, steps = [1e-4, 1e-8, 1e-12], 6
+    want_c, want_w = po.pcg_study(tols, steps, seed=0)
+    cold, warm, _, _ = pcg_study(tols, steps, seed=0, sequences=1, mode="parity")
+    assert np.array_equal(cold[..., 0], want_c) and np.array_equal(warm[..., 0], want_w)
