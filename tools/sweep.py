@@ -27,6 +27,7 @@ import paper_2510_06179_b200 as D  # noqa: E402
 from paper_2510_06179_b200 import _lib as L  # noqa: E402
 
 POOL = 65536
+CONVEX = False
 
 
 def hbm_peak():
@@ -39,15 +40,18 @@ def hbm_peak():
     return 6540.8
 
 
+NU = 4
+
+
 def run(T, B, reps, pool_cache):
-    prob = D.affine_quadratic(8, 4, T)
+    prob = D.affine_quadratic(8, NU, T)
     nz, nl = D.sizes(prob)
     if T not in pool_cache:
         pool_cache.clear()
-        pool_cache[T] = D.generate_affine_quadratic(8, 4, 0, min(B, POOL), convex=False)
+        pool_cache[T] = D.generate_affine_quadratic(8, NU, 0, min(B, POOL), convex=CONVEX)
     pool = pool_cache[T]
     if len(pool) < min(B, POOL):
-        pool = pool_cache[T] = D.generate_affine_quadratic(8, 4, 0, min(B, POOL), convex=False)
+        pool = pool_cache[T] = D.generate_affine_quadratic(8, NU, 0, min(B, POOL), convex=CONVEX)
     th = np.resize(pool, (B, pool.shape[1])) if B > len(pool) else pool[:B]
     b = D.Batch(prob, B)
     b.upload(L.F_THETA, th)
@@ -90,7 +94,11 @@ def main():
     ap.add_argument("--B", default="1024,4096,16384,65536")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--md", default=None)
+    ap.add_argument("--nu", type=int, default=4)
+    ap.add_argument("--convex", action="store_true", help="random_convex_instance draws (domain-randomised weights)")
     a = ap.parse_args()
+    global NU, CONVEX
+    NU, CONVEX = a.nu, a.convex
     rows = []
     cache = {}
     for T in [int(x) for x in a.T.split(",")]:
@@ -101,8 +109,9 @@ def main():
             torch.cuda.empty_cache()
     if a.md:
         with open(a.md, "w") as fh:
-            fh.write("# C5 sweep — solve + gradient on one B200 (FAST, cold caches, median of %d)\n\n" % a.reps)
-            fh.write("Workload: `random_linear_instance(8, 4, T)` draws, `sqp_solve` (5 SQP iterations max, "
+            fh.write("# Sweep — solve + gradient on one B200 (FAST, cold caches, median of %d)\n\n" % a.reps)
+            fh.write(f"Workload: `{'random_convex_instance' if CONVEX else 'random_linear_instance'}(8, {NU}, T)` "
+                     "draws, `sqp_solve` (5 SQP iterations max, "
                      "eps 1e-12) + `backward_vjp` per problem. PCG GB/s = algorithmic bytes "
                      "(SURVEY.md §8(d)) / PCG kernel time; HBM peak %.1f GB/s (MEASURED_PEAKS.json).\n\n" % hbm_peak())
             fh.write("| T | B | problems/s | ms/step | PCG it/solve | PCG share | PCG GB/s | x HBM | PCG kernel |\n")
