@@ -54,6 +54,15 @@ struct docp_batch {
   docp_dev::RolloutRec roll{};
   int roll_cap = -1;  // episode steps the record holds
   double roll_eps_pd = 1e-6;
+  // CUDA graphs of whole rollouts, replayed while their arguments and the
+  // batch's buffers (layout_gen) are unchanged
+  struct GraphCache {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<char> key;
+    uint64_t launches = 0;
+  };
+  GraphCache graph_fwd, graph_bwd;
+  uint64_t layout_gen = 0;  // bumped whenever a device buffer is reallocated
   // profiling: CUDA events around every launch, per kernel kind, on the batch stream
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof[DOCP_PROF_KINDS];
@@ -66,6 +75,8 @@ struct docp_batch {
   size_t pool_used = 0;
 
   ~docp_batch() {
+    if (graph_fwd.exec) cudaGraphExecDestroy(graph_fwd.exec);
+    if (graph_bwd.exec) cudaGraphExecDestroy(graph_bwd.exec);
     for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (h_count) cudaFreeHost(h_count);

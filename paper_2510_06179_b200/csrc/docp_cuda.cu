@@ -71,6 +71,7 @@ int dalloc(docp_batch* b, T** out, size_t count) {
 int ensure_hist(docp_batch* b, int n) {
   if (n <= b->max_hist) return DOCP_OK;
   int rc;
+  ++b->layout_gen;
   if ((rc = dalloc(b, &b->v.pcg_hist, static_cast<size_t>(b->B) * n))) return rc;
   if ((rc = dalloc(b, &b->v.step_sizes, static_cast<size_t>(b->B) * n))) return rc;
   b->max_hist = n;
@@ -712,6 +713,7 @@ int ensure_rollout(docp_batch* b, int H) {
   const Dims& d = b->d;
   const size_t B = static_cast<size_t>(b->B), h = static_cast<size_t>(H);
   int rc;
+  ++b->layout_gen;
   if ((rc = dalloc(b, &b->roll.z, h * B * d.nz)) || (rc = dalloc(b, &b->roll.lam, h * B * d.nl)) ||
       (rc = dalloc(b, &b->roll.x, (h + 1) * B * d.nx)) || (rc = dalloc(b, &b->roll.u, h * B * d.nu)))
     return rc;
@@ -719,6 +721,51 @@ int ensure_rollout(docp_batch* b, int H) {
   return DOCP_OK;
 }
 }  // namespace
+
+extern "C++" {
+namespace {
+/// Runs `body` (stream work only, no host synchronisation) through a cached
+/// CUDA graph when the batch has its own stream and is not profiling: the
+/// first call with a given key captures and instantiates, later calls replay.
+template <class F>
+int run_graph(docp_batch* b, docp_batch::GraphCache& gc, std::vector<char> key, F&& body) {
+  if (!b->stream || b->profiling || std::getenv("DOCP_NO_GRAPHS")) return body();
+  const char* gen = reinterpret_cast<const char*>(&b->layout_gen);
+  key.insert(key.end(), gen, gen + sizeof b->layout_gen);
+  if (!(gc.exec && gc.key == key)) {
+    if (gc.exec) {
+      cudaGraphExecDestroy(gc.exec);
+      gc.exec = nullptr;
+    }
+    const uint64_t l0 = g_launches.load();
+    CUDA_TRY(cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = body();
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(b->stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    CUDA_TRY(e);
+    const cudaError_t ei = cudaGraphInstantiate(&gc.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CUDA_TRY(ei);
+    gc.key = key;
+    gc.launches = g_launches.load() - l0;
+    g_launches.fetch_sub(gc.launches);  // counted when the graph runs
+  }
+  CUDA_TRY(cudaGraphLaunch(gc.exec, b->stream));
+  g_launches.fetch_add(gc.launches);
+  return DOCP_OK;
+}
+
+template <class T>
+void key_add(std::vector<char>& k, const T& v) {
+  const char* p = reinterpret_cast<const char*>(&v);
+  k.insert(k.end(), p, p + sizeof v);
+}
+}  // namespace
+}  // extern "C++"
 
 int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init, int32_t x_init_on_device,
                  int32_t H) {
@@ -729,48 +776,65 @@ int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init
   int rc = validate_sqp(cfg);
   if (rc) return rc;
   if ((rc = ensure_rollout(b, H))) return rc;
+  if ((rc = ensure_hist(b, std::max(1, cfg->max_sqp_iters)))) return rc;
   b->roll.H = H;
   b->roll_eps_pd = cfg->eps_pd;
-  if (!x_init_on_device) {  // stage the host states in the record's x_0 slot
-    CUDA_TRY(cudaMemcpyAsync(b->roll.x, x_init, sizeof(double) * b->B * b->d.nx, cudaMemcpyHostToDevice, b->stream));
-    x_init = b->roll.x;
-  }
-  const int g = grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8);
-  rollout_init_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, x_init);
-  LAUNCH_CHECK();
-  for (int t = 0; t < H; ++t) {
-    rollout_pre_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t);
+  // the initial states go to the record's x_0 slot first (outside any graph)
+  CUDA_TRY(cudaMemcpyAsync(b->roll.x, x_init, sizeof(double) * b->B * b->d.nx,
+                           x_init_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, b->stream));
+  auto body = [&]() -> int {
+    const int g = grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8);
+    rollout_init_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, b->roll.x);
     LAUNCH_CHECK();
-    if ((rc = docp_sqp_solve(b, cfg))) return rc;
-    rollout_post_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t);
-    LAUNCH_CHECK();
-  }
-  return DOCP_OK;
+    int r;
+    for (int t = 0; t < H; ++t) {
+      rollout_pre_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t);
+      LAUNCH_CHECK();
+      if ((r = docp_sqp_solve(b, cfg))) return r;
+      rollout_post_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t);
+      LAUNCH_CHECK();
+    }
+    return DOCP_OK;
+  };
+  // the SQP loop reads the active count back from iteration 4 on: only
+  // shorter solves are free of host synchronisation and can be captured
+  if (cfg->max_sqp_iters > 4) return body();
+  std::vector<char> key;
+  key_add(key, H);
+  key_add(key, *cfg);
+  return run_graph(b, b->graph_fwd, key, body);
 }
 
 int docp_rollout_backward(docp_batch* b, const docp_pcg_config* cfg) {
   if (!b || !cfg) return fail(DOCP_INVALID, "null argument");
   const int H = b->roll.H;
   if (H < 1 || b->roll_cap < H) return fail(DOCP_INVALID, "rollout_backward: no rollout recorded");
-  const int g = grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8);
-  rollout_back_init_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 256, b->num_sms * 8), 256, 0,
-                             b->stream>>>(b->v, b->roll);
-  LAUNCH_CHECK();
-  int rc;
-  for (int t = H - 1; t >= 0; --t) {
-    CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, sizeof(int), b->stream));
-    rollout_back_pre_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t, b->list[0], b->counts + 1);
+  auto body = [&]() -> int {
+    const int g = grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8);
+    rollout_back_init_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 256, b->num_sms * 8), 256, 0,
+                               b->stream>>>(b->v, b->roll);
     LAUNCH_CHECK();
-    // the step's cached matrices: re-linearised at its recorded solution
-    if ((rc = launch_assemble(b, b->list[0], b->counts + 1, b->B, b->roll_eps_pd, 1))) return rc;
-    if ((rc = docp_backward_vjp(b, cfg))) return rc;
-    rollout_back_post_kernel<<<grid_for(b->B, 128, b->num_sms * 4), 128, 0, b->stream>>>(b->v, b->roll, t);
+    int rc;
+    for (int t = H - 1; t >= 0; --t) {
+      CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, sizeof(int), b->stream));
+      rollout_back_pre_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t, b->list[0], b->counts + 1);
+      LAUNCH_CHECK();
+      // the step's cached matrices: re-linearised at its recorded solution
+      if ((rc = launch_assemble(b, b->list[0], b->counts + 1, b->B, b->roll_eps_pd, 1))) return rc;
+      if ((rc = docp_backward_vjp(b, cfg))) return rc;
+      rollout_back_post_kernel<<<grid_for(b->B, 128, b->num_sms * 4), 128, 0, b->stream>>>(b->v, b->roll, t);
+      LAUNCH_CHECK();
+    }
+    rollout_back_fini_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 256, b->num_sms * 8), 256, 0,
+                               b->stream>>>(b->v, b->roll);
     LAUNCH_CHECK();
-  }
-  rollout_back_fini_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 256, b->num_sms * 8), 256, 0,
-                             b->stream>>>(b->v, b->roll);
-  LAUNCH_CHECK();
-  return DOCP_OK;
+    return DOCP_OK;
+  };
+  std::vector<char> key;
+  key_add(key, H);
+  key_add(key, *cfg);
+  key_add(key, b->roll_eps_pd);
+  return run_graph(b, b->graph_bwd, key, body);
 }
 
 int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weights, int32_t learn_start,

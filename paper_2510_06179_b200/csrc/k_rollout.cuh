@@ -38,7 +38,7 @@ __global__ void rollout_init_kernel(View v, RolloutRec rr, const double* __restr
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < v.B; p += warps) {
     for (int e = lane; e < d.nz; e += 32) v.z[static_cast<long>(p) * d.nz + e] = 0.0;
     for (int e = lane; e < d.nl; e += 32) v.lam[static_cast<long>(p) * d.nl + e] = 0.0;
-    if (x_init != rr.x)
+    if (x_init != rr.x)  // (docp_rollout stages x_init in the record already)
       for (int e = lane; e < d.nx; e += 32) rr.x[static_cast<long>(p) * d.nx + e] = x_init[static_cast<long>(p) * d.nx + e];
     if (lane == 0) {
       rr.reward[p] = 0.0;

@@ -375,8 +375,15 @@ def test_rollout_affine_matches_reference(D, mode, one_step):
     b = D.Batch(D.affine_quadratic(nx, nu, T), B)
     b.upload(D._lib.F_THETA, th)
     xi = torch.tensor(x0, device="cuda")
-    b.rollout(gcfg, xi.data_ptr() if one_step else x0, H)  # device and host x_init paths
-    b.rollout_backward(gcfg.pcg)
+    # one_step: on a side stream, so the rollout and its backward run as captured CUDA graphs
+    # (second call replays them); otherwise eagerly on the default stream
+    side = torch.cuda.Stream() if one_step else None
+    if side is not None:
+        b.set_stream(side.cuda_stream)
+    for rep in range(2 if one_step else 1):
+        b.rollout(gcfg, xi.data_ptr() if one_step else x0, H)  # device and host x_init paths
+        b.rollout_backward(gcfg.pcg)
+    b.sync()
     got_r = b.download(D._lib.F_REWARD)[:, 0]
     got_g = b.download(D._lib.F_GRAD_THETA)
     errs = b.rollout_errors()

@@ -46,7 +46,7 @@ def gpu(nx, nu, T, B, reps):
     b = D.Batch(D.affine_quadratic(nx, nu, T), B)
     b.upload(L.F_THETA, th)
     cfg = D.SqpConfig(max_sqp_iters=1, step_candidates=[1.0], pcg=D.PcgConfig(epsilon=1e-12, mode="fast"))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a stream of its own: rollouts replay as CUDA graphs
     b.set_stream(stream.cuda_stream)
     fwd, both = [], []
     for rep in range(reps + 1):
