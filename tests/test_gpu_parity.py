@@ -480,3 +480,35 @@ def test_pcg_study_matches_reference(D):
     want_c, want_w = po.pcg_study(tols, steps, seed=0)
     cold, warm, _, _ = pcg_study(tols, steps, seed=0, sequences=1, mode="parity")
     assert np.array_equal(cold[..., 0], want_c) and np.array_equal(warm[..., 0], want_w)
+
+
+@pytest.mark.parametrize("nx,nu,T", [(8, 4, 256), (16, 8, 30), (8, 4, 100)])
+def test_pcg_breakdown_all_kernels(D, nx, nu, T):
+    """An indefinite diagonal block deep in the system: every FAST kernel
+    (single CTA, and the cluster forms whose CTAs must take the same
+    decision) reports the reference's BreakdownError at the oracle's
+    iteration, and the batch's other problems solve normally."""
+    th = aq_thetas(nx, nu, T, 31, 2)
+    pp = po.aq_problem(nx, nu, T)
+    o = po.Oracle("port", pp)
+    blocks, gammas = [], []
+    for j in range(2):
+        o.linearize(th[j], np.zeros(o.nz))
+        o.assemble()
+        blocks.append([np.array(a) for a in o.schur()])
+        gammas.append(o.gamma(o.flat_b(), o.flat_d()))
+    blocks[0][0][T // 2] = -blocks[0][0][T // 2]  # -S diag block of a mid-horizon stage
+    with pytest.raises(po.OracleError) as ei:
+        po.pcg_blocks("port", blocks[0][0], blocks[0][1], blocks[0][2], blocks[0][3], gammas[0], np.zeros(o.nl))
+    want_it = ei.value.iteration
+    want_ok = po.pcg_blocks("port", *blocks[1], gammas[1], np.zeros(o.nl))
+    b = D.Batch(D.affine_quadratic(nx, nu, T), 2)
+    b.upload_schur(*[np.stack([bl[k] for bl in blocks]) for k in range(4)])
+    b.upload(D._lib.F_GAMMA, np.stack(gammas))
+    for mode in ("parity", "fast"):
+        b.upload(D._lib.F_LAMBDA, np.zeros((2, b.nl)))
+        b.pcg_solve(D.PcgConfig(mode=mode))
+        errs = b.errors()
+        assert isinstance(errs[0], D.BreakdownError) and errs[0].iteration == want_it, (mode, errs[0])
+        assert errs[1] is None
+        assert b.download(D._lib.F_PCG_ITERS)[1, 0] == want_ok[1]
