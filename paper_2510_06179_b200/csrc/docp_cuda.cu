@@ -257,7 +257,9 @@ int launch_step(docp_batch* b, const docp_sqp_config& cfg, const int* list, cons
 }
 
 int launch_kkt(docp_batch* b, const int* list, const int* count, int n_hint) {
-  const size_t smem = static_cast<size_t>(b->d.nz + b->d.nl + b->d.nth) * sizeof(double);
+  const Dims& d = b->d;
+  const size_t smem =
+      static_cast<size_t>((d.T + 1) * (d.nx + d.nu + 1) + (d.T + 1) * (d.nx + 1) + d.nth) * sizeof(double);
   auto kern = kkt_kernel<0, 0>;
   const int nx = b->d.nx, nu = b->d.nu;
   if (nx == 8 && nu == 4) kern = kkt_kernel<8, 4>;

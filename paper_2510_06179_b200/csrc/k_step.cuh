@@ -36,9 +36,11 @@ struct StepCfg {
 /// to its slot (merit_parts throws at the first one in slot order).
 template <int NX, int NU>
 __device__ inline void merit_task(const Dims& d, const Family& fam, const double* th, const double* zo,
-                                  const double* zq, double alpha, bool trial, int task, double* slots,
+                                  const double* zq, int P, double alpha, bool trial, int task, double* slots,
                                   int* first_bad) {
   const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T;
+  auto xo = [&](int t) { return t * P; };       // x_t in the padded SMEM copy
+  auto uo = [&](int t) { return t * P + nx; };  // u_t
   constexpr int AX = NX ? NX : kMaxNx, AU = NU ? NU : kMaxNx;
   double a[AX], b[AU], c[AX], res[AX];
   auto get = [&](int off, int n, double* out) {
@@ -47,15 +49,15 @@ __device__ inline void merit_task(const Dims& d, const Family& fam, const double
       if (i < n) out[i] = trial ? zo[off + i] + alpha * (zq[off + i] - zo[off + i]) : zo[off + i];
   };
   if (task <= T) {
-    get(xoff(d, task), nx, a);
+    get(xo(task), nx, a);
     const double val = diag_cost_value<NX>(fam.scale, fam.w_x(d, th), a, nx);
     slots[task] = val;
     if (!isfinite(val)) atomicMin(first_bad, task);
   } else if (task < 2 * T + 1) {
     const int t = task - (T + 1);
-    get(xoff(d, t), nx, a);
-    get(uoff(d, t), nu, b);
-    get(xoff(d, t + 1), nx, c);
+    get(xo(t), nx, a);
+    get(uo(t), nu, b);
+    get(xo(t + 1), nx, c);
     const double val = diag_cost_value<NU>(fam.scale, fam.w_u(d, th), b, nu);
     slots[T + 1 + t] = val;
     if (!isfinite(val)) atomicMin(first_bad, T + 1 + t);
@@ -65,7 +67,7 @@ __device__ inline void merit_task(const Dims& d, const Family& fam, const double
     for (int i = 1; i < nx; ++i) s = s + fabs(res[i]);
     slots[2 * T + 1 + t] = s;
   } else {
-    get(xoff(d, 0), nx, a);
+    get(xo(0), nx, a);
     const double* x_s = fam.x_s(d, th);
     double s = fabs(a[0] - x_s[0]);
 #pragma unroll
@@ -93,8 +95,12 @@ __device__ inline void merit_fold(const Dims& d, const double* slots, double* co
 
 /// Dynamic shared memory of step_kernel (doubles): z_old, z_qp, theta, the
 /// merit slots of every version and the d_cost / curvature stage terms.
+/// z is staged with stage stride P = n_x + n_u + 1 (odd: the per-stage walks
+/// of consecutive threads land on distinct banks).
+__host__ __device__ inline int step_stride(const Dims& d) { return d.nx + d.nu + 1; }
 __host__ __device__ inline long step_smem_doubles(const Dims& d, int n_alpha) {
-  return 2L * d.nz + d.nth + static_cast<long>(n_alpha + 1) * (3 * d.T + 2) + 2L * (2 * d.T + 1);
+  const long zs = static_cast<long>(d.T + 1) * step_stride(d);
+  return 2L * zs + d.nth + static_cast<long>(n_alpha + 1) * (3 * d.T + 2) + 2L * (2 * d.T + 1);
 }
 
 /// K3: line search from Z toward Z_QP and the SQP-loop bookkeeping
@@ -116,9 +122,11 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
   const int tid = threadIdx.x;
   const int nslot = 3 * T + 2;
   const int nver = cfg.n_alpha + 1;
-  double* szo = sm_step;                                   // [nz]
-  double* szq = szo + d.nz;                                // [nz]
-  double* sth = szq + d.nz;                                // [nth]
+  const int P = step_stride(d);
+  const int zs = (T + 1) * P;
+  double* szo = sm_step;                                   // [T+1][P] padded stages
+  double* szq = szo + zs;                                  // [T+1][P]
+  double* sth = szq + zs;                                  // [nth]
   double* slots = sth + d.nth;                             // [nver][nslot]
   double* dterm = slots + static_cast<long>(nver) * nslot;  // [2T+1] d_cost terms
   double* cterm = dterm + 2 * T + 1;                       // [2T+1] curvature terms
@@ -131,8 +139,9 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
       const double* th = v.theta + static_cast<long>(p) * d.nth;
       const double* zq = v.zqp + static_cast<long>(p) * d.nz;
       for (int e = tid; e < d.nz; e += blockDim.x) {
-        szo[e] = zo[e];
-        szq[e] = zq[e];
+        const int t = e / (nx + nu), c = e - t * (nx + nu);
+        szo[t * P + c] = zo[e];
+        szq[t * P + c] = zq[e];
       }
       for (int e = tid; e < d.nth; e += blockDim.x) sth[e] = th[e];
       if (tid < nver) s_bad[tid] = 0x7fffffff;
@@ -147,7 +156,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
       const bool st = t <= T;
       const int s = st ? t : t - (T + 1);
       const int n = st ? nx : nu;
-      const int off = st ? xoff(d, s) : uoff(d, s);
+      const int off = st ? s * P : s * P + nx;
       const double* wt = st ? fam.w_x(d, sth) : fam.w_u(d, sth);
       const double* h = st ? qd + s * nx : rd + s * nu;
       double dc = 0.0, cv = 0.0;
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
     for (int task = tid; task < nver * (2 * T + 2); task += blockDim.x) {
       const int ver = task / (2 * T + 2);
       const int tt = task - ver * (2 * T + 2);
-      merit_task<NX, NU>(d, fam, sth, szo, szq, ver == 0 ? 0.0 : cfg.alphas[ver - 1], ver > 0, tt,
+      merit_task<NX, NU>(d, fam, sth, szo, szq, P, ver == 0 ? 0.0 : cfg.alphas[ver - 1], ver > 0, tt,
                          slots + static_cast<long>(ver) * nslot, &s_bad[ver]);
     }
     __syncthreads();
@@ -236,16 +245,20 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
     // z_new = z_old.interpolate(z_qp, alpha) and the step norm (trajectory.hpp:57-68)
     double stepmax = 0.0;
     for (int e = tid; e < d.nz; e += blockDim.x) {
-      const double zn = szo[e] + alpha * (szq[e] - szo[e]);
+      const int t = e / (nx + nu), k = t * P + (e - t * (nx + nu));
+      const double zn = szo[k] + alpha * (szq[k] - szo[k]);
       if (!isfinite(zn)) s_nonfinite = 1;
-      stepmax = fmax(stepmax, fabs(zn - szo[e]));
+      stepmax = fmax(stepmax, fabs(zn - szo[k]));
     }
     stepmax = warp_max(stepmax);
     if ((tid & 31) == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_step), __double_as_longlong(stepmax));
     __syncthreads();
     const bool diverged = s_nonfinite != 0;
     if (!diverged)
-      for (int e = tid; e < d.nz; e += blockDim.x) zo[e] = szo[e] + alpha * (szq[e] - szo[e]);
+      for (int e = tid; e < d.nz; e += blockDim.x) {
+        const int t = e / (nx + nu), k = t * P + (e - t * (nx + nu));
+        zo[e] = szo[k] + alpha * (szq[k] - szo[k]);
+      }
     if (tid == 0) {
       v.mu[p] = s_mu;
       v.alpha[p] = alpha;
@@ -276,15 +289,21 @@ __global__ void __launch_bounds__(kKktThreads) kkt_kernel(View v, const int* __r
   const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T;
   constexpr int AX = NX ? NX : kMaxNx, AU = NU ? NU : kMaxNx;
   const Family fam = Family::from(v.prob);
-  double* z = sm_kkt;          // [nz]
-  double* lam = z + d.nz;      // [nl]
-  double* th = lam + d.nl;     // [nth]
+  // padded copies (odd strides: consecutive threads' stage walks hit distinct banks)
+  const int P = nx + nu + 1, Q = nx + 1;
+  double* z = sm_kkt;                 // [T+1][P]: x_t at t P, u_t at t P + n_x
+  double* lam = z + (T + 1) * P;      // [T+1][Q]
+  double* th = lam + (T + 1) * Q;     // [nth]
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
     if (v.status[p].code != DOCP_OK) continue;
     if (threadIdx.x == 0) s_max = 0ull;
-    for (int e = threadIdx.x; e < d.nz; e += blockDim.x) z[e] = v.z[static_cast<long>(p) * d.nz + e];
-    for (int e = threadIdx.x; e < d.nl; e += blockDim.x) lam[e] = v.lam[static_cast<long>(p) * d.nl + e];
+    for (int e = threadIdx.x; e < d.nz; e += blockDim.x) {
+      const int t = e / (nx + nu);
+      z[t * P + (e - t * (nx + nu))] = v.z[static_cast<long>(p) * d.nz + e];
+    }
+    for (int e = threadIdx.x; e < d.nl; e += blockDim.x)
+      lam[(e / nx) * Q + e % nx] = v.lam[static_cast<long>(p) * d.nl + e];
     for (int e = threadIdx.x; e < d.nth; e += blockDim.x) th[e] = v.theta[static_cast<long>(p) * d.nth + e];
     __syncthreads();
     double m = 0.0;
@@ -292,23 +311,23 @@ __global__ void __launch_bounds__(kKktThreads) kkt_kernel(View v, const int* __r
       double jx[AX * AX], ju[AX * AU], res[AX];
       const double* wx = fam.w_x(d, th);
       // grad_l for x_t: cost grad, + lambda_t (A+_{t-1}' lambda_t, or lambda_0 last), + A_t' lambda_{t+1}
-      if (t < T) fam.dynamics<NX, NU>(d, th, z + xoff(d, t + 1), z + xoff(d, t), z + uoff(d, t), res, jx, ju);
+      if (t < T) fam.dynamics<NX, NU>(d, th, z + (t + 1) * P, z + t * P, z + t * P + nx, res, jx, ju);
 #pragma unroll
       for (int i = 0; i < AX; ++i) {
         if (i >= nx) break;
-        double g = diag_cost_grad(fam.scale, wx[i], z[xoff(d, t) + i]);
+        double g = diag_cost_grad(fam.scale, wx[i], z[t * P + i]);
         double a = 0.0;
         if (t < T) {
-          a = jx[i * nx] * lam[(t + 1) * nx];
+          a = jx[i * nx] * lam[(t + 1) * Q];
 #pragma unroll
           for (int k = 1; k < AX; ++k)
-            if (k < nx) a = a + jx[k + i * nx] * lam[(t + 1) * nx + k];
+            if (k < nx) a = a + jx[k + i * nx] * lam[(t + 1) * Q + k];
         }
         if (t == 0) {
           if (t < T) g = g + a;
           g = g + lam[i];
         } else {
-          g = g + lam[t * nx + i];
+          g = g + lam[t * Q + i];
           if (t < T) g = g + a;
         }
         m = fmax(m, fabs(g));
@@ -318,11 +337,11 @@ __global__ void __launch_bounds__(kKktThreads) kkt_kernel(View v, const int* __r
 #pragma unroll
         for (int i = 0; i < AU; ++i) {
           if (i >= nu) break;
-          double g = diag_cost_grad(fam.scale, wu[i], z[uoff(d, t) + i]);
-          double a = ju[i * nx] * lam[(t + 1) * nx];
+          double g = diag_cost_grad(fam.scale, wu[i], z[t * P + nx + i]);
+          double a = ju[i * nx] * lam[(t + 1) * Q];
 #pragma unroll
           for (int k = 1; k < AX; ++k)
-            if (k < nx) a = a + ju[k + i * nx] * lam[(t + 1) * nx + k];
+            if (k < nx) a = a + ju[k + i * nx] * lam[(t + 1) * Q + k];
           m = fmax(m, fabs(g + a));
         }
 #pragma unroll
