@@ -236,16 +236,18 @@ int launch_step(docp_batch* b, const docp_sqp_config& cfg, const int* list, cons
   sc.iter = iter;
   sc.max_iters = cfg.max_sqp_iters;
   sc.is_loop = is_loop;
-  const size_t smem = static_cast<size_t>(step_smem_doubles(b->d, sc.n_alpha)) * sizeof(double);
   int max_optin = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device));
+  const bool stage = (step_smem_doubles(b->d, sc.n_alpha, true) * sizeof(double) + 1024) <= static_cast<size_t>(max_optin);
+  const size_t smem = static_cast<size_t>(step_smem_doubles(b->d, sc.n_alpha, stage)) * sizeof(double);
   if (smem + 1024 > static_cast<size_t>(max_optin)) return fail(DOCP_UNSUPPORTED, "line search: horizon too long");
-  auto kern = step_kernel<0, 0>;
   const int nx = b->d.nx, nu = b->d.nu;
-  if (nx == 8 && nu == 4) kern = step_kernel<8, 4>;
-  else if (nx == 8 && nu == 2) kern = step_kernel<8, 2>;
-  else if (nx == 4 && nu == 2) kern = step_kernel<4, 2>;
-  else if (nx == 4 && nu == 1) kern = step_kernel<4, 1>;
+  auto kern = stage ? step_kernel<0, 0, true> : step_kernel<0, 0, false>;
+  if (nx == 8 && nu == 4) kern = stage ? step_kernel<8, 4, true> : step_kernel<8, 4, false>;
+  else if (nx == 8 && nu == 2) kern = stage ? step_kernel<8, 2, true> : step_kernel<8, 2, false>;
+  else if (nx == 4 && nu == 2) kern = step_kernel<4, 2, true>;
+  else if (nx == 4 && nu == 1) kern = step_kernel<4, 1, true>;
+  if (!stage && ((nx == 4 && nu == 2) || (nx == 4 && nu == 1))) kern = step_kernel<0, 0, false>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem));
@@ -260,6 +262,9 @@ int launch_kkt(docp_batch* b, const int* list, const int* count, int n_hint) {
   const Dims& d = b->d;
   const size_t smem =
       static_cast<size_t>((d.T + 1) * (d.nx + d.nu + 1) + (d.T + 1) * (d.nx + 1) + d.nth) * sizeof(double);
+  int max_optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device));
+  if (smem + 1024 > static_cast<size_t>(max_optin)) return fail(DOCP_UNSUPPORTED, "kkt_residual: horizon too long");
   auto kern = kkt_kernel<0, 0>;
   const int nx = b->d.nx, nu = b->d.nu;
   if (nx == 8 && nu == 4) kern = kkt_kernel<8, 4>;

@@ -97,10 +97,12 @@ __device__ inline void merit_fold(const Dims& d, const double* slots, double* co
 /// merit slots of every version and the d_cost / curvature stage terms.
 /// z is staged with stage stride P = n_x + n_u + 1 (odd: the per-stage walks
 /// of consecutive threads land on distinct banks).
+/// Long horizons whose staged copies do not fit read z and theta from global
+/// memory instead (STAGE = false), keeping only the merit slots in SMEM.
 __host__ __device__ inline int step_stride(const Dims& d) { return d.nx + d.nu + 1; }
-__host__ __device__ inline long step_smem_doubles(const Dims& d, int n_alpha) {
-  const long zs = static_cast<long>(d.T + 1) * step_stride(d);
-  return 2L * zs + d.nth + static_cast<long>(n_alpha + 1) * (3 * d.T + 2) + 2L * (2 * d.T + 1);
+__host__ __device__ inline long step_smem_doubles(const Dims& d, int n_alpha, bool stage = true) {
+  const long zs = stage ? static_cast<long>(d.T + 1) * step_stride(d) : 0;
+  return 2L * zs + (stage ? d.nth : 0) + static_cast<long>(n_alpha + 1) * (3 * d.T + 2) + 2L * (2 * d.T + 1);
 }
 
 /// K3: line search from Z toward Z_QP and the SQP-loop bookkeeping
@@ -108,7 +110,7 @@ __host__ __device__ inline long step_smem_doubles(const Dims& d, int n_alpha) {
 /// z_qp and theta are staged in shared memory, the stage terms of every
 /// version are evaluated in parallel, and each sum is folded by one thread
 /// in the reference's order. NX, NU > 0 fix the block sizes at compile time.
-template <int NX, int NU>
+template <int NX, int NU, bool STAGE = true>
 __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* __restrict__ work,
                                                            const int* __restrict__ n_work, StepCfg cfg) {
   extern __shared__ double sm_step[];
@@ -122,12 +124,12 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
   const int tid = threadIdx.x;
   const int nslot = 3 * T + 2;
   const int nver = cfg.n_alpha + 1;
-  const int P = step_stride(d);
-  const int zs = (T + 1) * P;
-  double* szo = sm_step;                                   // [T+1][P] padded stages
+  const int P = STAGE ? step_stride(d) : nx + nu;  // stage stride of the z copies read below
+  const int zs = STAGE ? (T + 1) * P : 0;
+  double* szo = sm_step;                                   // [T+1][P] padded stages (STAGE)
   double* szq = szo + zs;                                  // [T+1][P]
   double* sth = szq + zs;                                  // [nth]
-  double* slots = sth + d.nth;                             // [nver][nslot]
+  double* slots = sth + (STAGE ? d.nth : 0);               // [nver][nslot]
   double* dterm = slots + static_cast<long>(nver) * nslot;  // [2T+1] d_cost terms
   double* cterm = dterm + 2 * T + 1;                       // [2T+1] curvature terms
 
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
     const int p = work[w];
     if (v.status[p].code != DOCP_OK) continue;
     double* zo = v.z + static_cast<long>(p) * d.nz;
-    {
+    if constexpr (STAGE) {
       const double* th = v.theta + static_cast<long>(p) * d.nth;
       const double* zq = v.zqp + static_cast<long>(p) * d.nz;
       for (int e = tid; e < d.nz; e += blockDim.x) {
@@ -144,8 +146,12 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
         szq[t * P + c] = zq[e];
       }
       for (int e = tid; e < d.nth; e += blockDim.x) sth[e] = th[e];
-      if (tid < nver) s_bad[tid] = 0x7fffffff;
+    } else {  // the flat layout has the same stage stride: read in place
+      szo = zo;
+      szq = v.zqp + static_cast<long>(p) * d.nz;
+      sth = v.theta + static_cast<long>(p) * d.nth;
     }
+    if (tid < nver) s_bad[tid] = 0x7fffffff;
     __syncthreads();
     const double* qd = v.qd + static_cast<long>(p) * d.nb * nx;
     const double* rd = v.rd + static_cast<long>(p) * T * nu;

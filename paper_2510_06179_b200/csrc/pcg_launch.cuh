@@ -30,7 +30,11 @@ int launch_pcg_r(docp_batch* b, const PcgPlan& pl, const int* list, const int* c
   switch (pl.maxr) {
     case 1: return launch_pcg_t<NX, 1, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
     case 2: return launch_pcg_t<NX, 2, PAR, RES>(b, pl, list, count, n_hint, sol, eps, max_iters);
-    default: return fail(DOCP_UNSUPPORTED, "pcg: horizon %d too long (max 2047)", b->d.T);
+    default:
+      return fail(DOCP_UNSUPPORTED,
+                  "pcg: horizon %d too long for the one-thread-per-block-row kernel (T <= 511; FAST n_x = 8 / 16 "
+                  "runs longer horizons on thread-block clusters)",
+                  b->d.T);
   }
 }
 
