@@ -244,7 +244,7 @@ __device__ double block_norm(const double (&a)[MAXB][NN], const int (&bi)[MAXB],
 
 /// K2. NX in {4, 8, 16}: compile-time block size; NX == 0: any n_x <= 16.
 template <int NX, int MAXB, bool PAR, bool RESIDENT>
-__global__ void __launch_bounds__(kPcgMaxThreads) pcg_kernel(View v, const int* __restrict__ work,
+__global__ void __launch_bounds__(kPcgMaxThreads, (NX == 4 && MAXB == 1 && !PAR) ? 2 : 1) pcg_kernel(View v, const int* __restrict__ work,
                                                             const int* __restrict__ n_work, int* __restrict__ counter,
                                                             double* __restrict__ sol_all, double epsilon,
                                                             int max_iters_cfg) {

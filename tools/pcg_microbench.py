@@ -38,3 +38,4 @@ def run(nx, nu, T, B, modes=("fast", "parity"), caps=(1, 11, 41)):
 run(8, 4, 100, 1184)
 run(8, 4, 30, 1184)
 run(4, 2, 20, 1184, modes=("fast",))
+run(4, 1, 50, 4096, modes=("fast", "parity"))
