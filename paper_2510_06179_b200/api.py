@@ -253,7 +253,10 @@ class Batch:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            L.lib().docp_batch_destroy(h)
+            try:
+                L.lib().docp_batch_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     # ---- data

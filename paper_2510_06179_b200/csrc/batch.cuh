@@ -129,6 +129,8 @@ struct PcgPlan {
   int name(docp_batch* b, const PcgPlan& pl, bool par, const int* list, const int* count, int n_hint, double* sol, \
            double eps, int max_iters)
 DOCP_PCG_LAUNCHER(launch_pcg_nx4);
+/// Whether FAST n_x = 4 solves of this shape run pcg_kernel_h4f.
+bool h4f_fits(const docp_dev::Dims& d, int device);
 DOCP_PCG_LAUNCHER(launch_pcg_nx16);
 int h16f_cluster_for(const docp_dev::Dims& d, int device);
 /// Cluster size pcg_kernel_h8f uses for this batch's shape (0: not used).

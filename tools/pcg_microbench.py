@@ -35,7 +35,12 @@ def run(nx, nu, T, B, modes=("fast", "parity"), caps=(1, 11, 41)):
                           "us_per_iter_per_SM": slope * 1e3 / waves,
                           "cycles_per_iter@1.965GHz": slope * 1e-3 / waves * 1.965e9}), flush=True)
 
-run(8, 4, 100, 1184)
-run(8, 4, 30, 1184)
-run(4, 2, 20, 1184, modes=("fast",))
-run(4, 1, 50, 4096, modes=("fast", "parity"))
+if __name__ == "__main__":
+    if "--nx4" in sys.argv:
+        run(4, 2, 20, 1184, modes=("fast",))
+        run(4, 1, 50, 4096, modes=("fast",))
+    else:
+        run(8, 4, 100, 1184)
+        run(8, 4, 30, 1184)
+        run(4, 2, 20, 1184, modes=("fast",))
+        run(4, 1, 50, 4096, modes=("fast", "parity"))
