@@ -4,6 +4,7 @@
 
 #include "k_pcg_h8.cuh"
 #include "k_pcg_h8f.cuh"
+#include "k_pcg_h8r.cuh"
 #include "pcg_launch.cuh"
 
 namespace docp_host {
@@ -65,14 +66,36 @@ int launch_h8f_cl(docp_batch* b, const int* list, const int* count, int n_hint, 
   return DOCP_OK;
 }
 
+/// FAST, one CTA per problem: pcg_kernel_h8r (-S in registers, next
+/// problem's -S prefetched into shared memory).
+static int launch_h8r(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
+                      int max_iters) {
+  auto kern = pcg_kernel_h8r<256>;
+  const size_t smem = h8r_smem_doubles(b->d) * sizeof(double);
+  const int threads = (2 * b->d.nb + 31) / 32 * 32;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit on an SM (smem %zu)", smem);
+  const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
+  CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
+  ProfScope ps(b, DOCP_PROF_PCG);
+  kern<<<grid, threads, smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
 /// Smallest cluster (1, 2, 4, 8) whose per-CTA share of the blocks fits in
 /// shared memory with at most 128 block rows per CTA; 0 if none.
 int h8f_cluster_for(const Dims& d, int device) {
   if (d.nx != 8) return 0;
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  int min_cl = 1;  // DOCP_H8F_CLUSTER=c: A/B override, smallest cluster size tried
+  if (const char* e = std::getenv("DOCP_H8F_CLUSTER")) min_cl = std::atoi(e);
   for (int cl : {1, 2, 4, 8}) {
     if (cl > 1 && (cl - 1) * h8f_rows(d, cl) >= d.nb) break;  // every CTA must own a row
+    if (cl < min_cl) continue;
     if (h8f_rows(d, cl) <= 128 && h8f_smem_doubles(d, cl) * 8 + 64 <= static_cast<long>(max_optin)) return cl;
   }
   return 0;
@@ -81,10 +104,11 @@ static int h8f_cluster(const docp_batch* b) { return h8f_cluster_for(b->d, b->de
 
 /// Kernel variant override for A/B measurements: DOCP_PCG_VARIANT=h8 keeps
 /// FAST solves on pcg_kernel_h8.
-static bool force_h8() {
+static bool force_variant(const char* name) {
   const char* e = std::getenv("DOCP_PCG_VARIANT");
-  return e && std::strcmp(e, "h8") == 0;
+  return e && std::strcmp(e, name) == 0;
 }
+static bool force_h8() { return force_variant("h8"); }
 
 /// n_x = 8: FAST -> pcg_kernel_h8f on the smallest cluster that keeps the
 /// blocks on-chip; PARITY (or no fitting cluster): two threads per block row
@@ -92,7 +116,9 @@ static bool force_h8() {
 DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
   if (!par && !force_h8()) {
     switch (h8f_cluster(b)) {
-      case 1: return launch_h8f_cl<1>(b, list, count, n_hint, sol, eps, max_iters);
+      case 1:
+        if (!force_variant("h8f")) return launch_h8r(b, list, count, n_hint, sol, eps, max_iters);
+        return launch_h8f_cl<1>(b, list, count, n_hint, sol, eps, max_iters);
       case 2: return launch_h8f_cl<2>(b, list, count, n_hint, sol, eps, max_iters);
       case 4: return launch_h8f_cl<4>(b, list, count, n_hint, sol, eps, max_iters);
       case 8: return launch_h8f_cl<8>(b, list, count, n_hint, sol, eps, max_iters);
