@@ -135,10 +135,11 @@ __global__ void reset_status_kernel(View v) {
 
 // ---------------------------------------------------------------- launch helpers
 template <int NX, int NU, int TH>
-int launch_assemble_th(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur) {
+int launch_assemble_th(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur,
+                       bool fast) {
   constexpr int NG = TH / NX;
   const size_t smem = static_cast<size_t>(NG) * AsmLayout<NX, NU>::GBUF * sizeof(double);
-  auto kern = assemble_kernel_t<NX, NU, TH>;
+  auto kern = fast ? assemble_kernel_t<NX, NU, TH, true> : assemble_kernel_t<NX, NU, TH, false>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TH, smem));
@@ -152,17 +153,22 @@ int launch_assemble_th(docp_batch* b, const int* list, const int* count, int n_h
 /// 128 threads: 16 groups of 8 lanes (n_x = 8). A 160-thread variant (whole
 /// rounds at T = 100) measured 3% slower: occupancy fell from 16 to 15 warps/SM.
 template <int NX, int NU>
-int launch_assemble_t(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur) {
-  return launch_assemble_th<NX, NU, kAsmGroupThreads>(b, list, count, n_hint, eps_pd, do_schur);
+int launch_assemble_t(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur,
+                      bool fast) {
+  return launch_assemble_th<NX, NU, kAsmGroupThreads>(b, list, count, n_hint, eps_pd, do_schur, fast);
 }
 
-int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur) {
+/// K1. fast (PCG mode FAST): reciprocal / fma arithmetic in the compile-time
+/// shapes (assemble_kernel_t<..., true>); the runtime-shape kernel is always
+/// the reference's arithmetic.
+int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur,
+                    bool fast = false) {
   const int nx = b->d.nx, nu = b->d.nu;
-  if (nx == 8 && nu == 4) return launch_assemble_t<8, 4>(b, list, count, n_hint, eps_pd, do_schur);
-  if (nx == 8 && nu == 2) return launch_assemble_t<8, 2>(b, list, count, n_hint, eps_pd, do_schur);
-  if (nx == 4 && nu == 2) return launch_assemble_t<4, 2>(b, list, count, n_hint, eps_pd, do_schur);
-  if (nx == 4 && nu == 1) return launch_assemble_t<4, 1>(b, list, count, n_hint, eps_pd, do_schur);
-  if (nx == 16 && nu == 8) return launch_assemble_t<16, 8>(b, list, count, n_hint, eps_pd, do_schur);
+  if (nx == 8 && nu == 4) return launch_assemble_t<8, 4>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  if (nx == 8 && nu == 2) return launch_assemble_t<8, 2>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  if (nx == 4 && nu == 2) return launch_assemble_t<4, 2>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  if (nx == 4 && nu == 1) return launch_assemble_t<4, 1>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  if (nx == 16 && nu == 8) return launch_assemble_t<16, 8>(b, list, count, n_hint, eps_pd, do_schur, fast);
   const int sp = std::max(b->d.bsz, b->d.nx * b->d.nu);
   const size_t smem = static_cast<size_t>(kAsmWarps) * 6 * sp * sizeof(double);
   CUDA_TRY(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -669,7 +675,7 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
   for (int iter = 0; iter < cfg->max_sqp_iters && n_bound > 0; ++iter) {
     const int* list = b->list[cur];
     const int* cnt = b->counts + 1 + cur;
-    if ((rc = launch_assemble(b, list, cnt, n_bound, cfg->eps_pd, 1))) return rc;
+    if ((rc = launch_assemble(b, list, cnt, n_bound, cfg->eps_pd, 1, cfg->pcg.mode == DOCP_PCG_FAST))) return rc;
     if ((rc = launch_gamma(b, list, cnt, n_bound, DOCP_RHS_FORWARD))) return rc;
     if ((rc = launch_pcg(b, cfg->pcg, list, cnt, n_bound, b->v.lam))) return rc;
     if ((rc = launch_recover(b, list, cnt, n_bound, b->v.lam, DOCP_RHS_FORWARD))) return rc;
@@ -690,7 +696,7 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
   int* fin_cnt = b->counts + 1 + (cur ^ 1);
   ok_list_kernel<<<grid_for(b->B, 256, 4096), 256, 0, b->stream>>>(b->v, fin, fin_cnt);
   LAUNCH_CHECK();
-  if ((rc = launch_assemble(b, fin, fin_cnt, b->B, cfg->eps_pd, 1))) return rc;
+  if ((rc = launch_assemble(b, fin, fin_cnt, b->B, cfg->eps_pd, 1, cfg->pcg.mode == DOCP_PCG_FAST))) return rc;
   if ((rc = launch_kkt(b, fin, fin_cnt, b->B))) return rc;
   return DOCP_OK;
 }
@@ -827,7 +833,8 @@ int docp_rollout_backward(docp_batch* b, const docp_pcg_config* cfg) {
       rollout_back_pre_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t, b->list[0], b->counts + 1);
       LAUNCH_CHECK();
       // the step's cached matrices: re-linearised at its recorded solution
-      if ((rc = launch_assemble(b, b->list[0], b->counts + 1, b->B, b->roll_eps_pd, 1))) return rc;
+      if ((rc = launch_assemble(b, b->list[0], b->counts + 1, b->B, b->roll_eps_pd, 1, cfg->mode == DOCP_PCG_FAST)))
+        return rc;
       if ((rc = docp_backward_vjp(b, cfg))) return rc;
       rollout_back_post_kernel<<<grid_for(b->B, 128, b->num_sms * 4), 128, 0, b->stream>>>(b->v, b->roll, t);
       LAUNCH_CHECK();

@@ -386,7 +386,14 @@ struct AsmLayout {
 
 /// TH threads per CTA (TH / NX stage groups); the launcher picks TH so that the
 /// groups divide the horizon's stages into whole rounds where it can.
-template <int NX, int NU, int TH>
+///
+/// FAST = true (PCG mode FAST): the same blocks up to rounding, with the
+/// reference's divisions replaced by reciprocals — M1/M2 scale columns by
+/// 1/q_k, 1/r_k (q, r the projected cost diagonals), the Cholesky of chi_t
+/// takes 1/l_kk = rsqrt(pivot) and keeps it on the factor's diagonal for the
+/// triangular solves — and fma accumulation. FAST = false is the
+/// reference's arithmetic bit for bit.
+template <int NX, int NU, int TH, bool FAST>
 __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assemble_kernel_t(View v, const int* __restrict__ work,
                                                                       const int* __restrict__ n_work, double eps_pd,
                                                                       int do_schur) {
@@ -436,6 +443,8 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
     }
     const double* lq = v.lq + static_cast<long>(p) * d.nb * NX;
     const double* lr = v.lr + static_cast<long>(p) * T * NU;
+    const double* qdp = v.qd + static_cast<long>(p) * d.nb * NX;
+    const double* rdp = v.rd + static_cast<long>(p) * T * NU;
     double* blk = blk_ptr(v, p);
     double* Sd = blk + d.s_diag;
     double* Ss = blk + d.s_sub;
@@ -456,22 +465,42 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
       for (int k = l; k < NX * NU; k += NX) sB[ix(k % NX, k / NX)] = Bt[k];
       __syncwarp(gmask);
       // M1(k, l) = (A(l,k)/lq_k)/lq_k ; M2(k, l) = (B(l,k)/lr_k)/lr_k
+      double c3, dq;
+      if constexpr (FAST) {  // lane k scales column k of A (of B) by 1/q_k (1/r_k)
+        dq = __drcp_rn(qdp[t * NX + l]);
+        c3 = __drcp_rn(qdp[(t + 1) * NX + l]);
 #pragma unroll
-      for (int k = 0; k < NX; ++k) sM1[ix(k, l)] = (sA[ix(l, k)] / lqt[k]) / lqt[k];
+        for (int j = 0; j < NX; ++j) sM1[ix(l, j)] = sA[ix(j, l)] * dq;
+        if (l < NU) {
+          const double ir = __drcp_rn(rdp[t * NU + l]);
 #pragma unroll
-      for (int k = 0; k < NU; ++k) sM2[iu(k, l)] = (sB[ix(l, k)] / lrt[k]) / lrt[k];
+          for (int j = 0; j < NX; ++j) sM2[iu(l, j)] = sB[ix(j, l)] * ir;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NX; ++k) sM1[ix(k, l)] = (sA[ix(l, k)] / lqt[k]) / lqt[k];
+#pragma unroll
+        for (int k = 0; k < NU; ++k) sM2[iu(k, l)] = (sB[ix(l, k)] / lrt[k]) / lrt[k];
+        c3 = (1.0 / lqn[l]) / lqn[l];
+        dq = (1.0 / lqt[l]) / lqt[l];
+      }
       __syncwarp(gmask);
       // column l of chi = A M1 + B M2 + A+ Q+^-1 A+'  and of phi_t = A Q_t^-1
-      const double c3 = (1.0 / lqn[l]) / lqn[l];
-      const double dq = (1.0 / lqt[l]) / lqt[l];
 #pragma unroll
       for (int i = 0; i < NX; ++i) {
         double a = sA[ix(i, 0)] * sM1[ix(0, l)];
-#pragma unroll
-        for (int m = 1; m < NX; ++m) a = a + sA[ix(i, m)] * sM1[ix(m, l)];
         double b = sB[ix(i, 0)] * sM2[iu(0, l)];
+        if constexpr (FAST) {
 #pragma unroll
-        for (int m = 1; m < NU; ++m) b = b + sB[ix(i, m)] * sM2[iu(m, l)];
+          for (int m = 1; m < NX; ++m) a = fma(sA[ix(i, m)], sM1[ix(m, l)], a);
+#pragma unroll
+          for (int m = 1; m < NU; ++m) b = fma(sB[ix(i, m)], sM2[iu(m, l)], b);
+        } else {
+#pragma unroll
+          for (int m = 1; m < NX; ++m) a = a + sA[ix(i, m)] * sM1[ix(m, l)];
+#pragma unroll
+          for (int m = 1; m < NU; ++m) b = b + sB[ix(i, m)] * sM2[iu(m, l)];
+        }
         sC[ix(i, l)] = (a + b) + (i == l ? c3 : 0.0);
       }
       __syncwarp(gmask);  // B_t / M2 are dead: sO takes their place
@@ -495,23 +524,24 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
         if (k > 0) {
           s = sL[ix(k, 0)] * sL[ix(k, 0)];
 #pragma unroll
-          for (int j = 1; j < k; ++j) s = s + sL[ix(k, j)] * sL[ix(k, j)];
+          for (int j = 1; j < k; ++j) s = FAST ? fma(sL[ix(k, j)], sL[ix(k, j)], s) : s + sL[ix(k, j)] * sL[ix(k, j)];
         }
         const double piv = sD[ix(k, k)] - s;
         if (piv <= 0.0) {
           failed = true;
           break;
         }
-        const double lk = sqrt(piv);
+        // FAST: the factor's diagonal holds 1/l_kk (only the solves read it)
+        const double lk = FAST ? rsqrt(piv) : sqrt(piv);
         if (l == k) sL[ix(k, k)] = lk;
         if (l > k) {
           double tt = 0.0;
           if (k > 0) {
             tt = sL[ix(l, 0)] * sL[ix(k, 0)];
 #pragma unroll
-            for (int j = 1; j < k; ++j) tt = tt + sL[ix(l, j)] * sL[ix(k, j)];
+            for (int j = 1; j < k; ++j) tt = FAST ? fma(sL[ix(l, j)], sL[ix(k, j)], tt) : tt + sL[ix(l, j)] * sL[ix(k, j)];
           }
-          sL[ix(l, k)] = (sD[ix(l, k)] - tt) / lk;
+          sL[ix(l, k)] = FAST ? (sD[ix(l, k)] - tt) * lk : (sD[ix(l, k)] - tt) / lk;
         }
         __syncwarp(gmask);
       }
@@ -530,9 +560,9 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
           if (i > 0) {
             s = sL[ix(i, 0)] * x[0];
 #pragma unroll
-            for (int j = 1; j < i; ++j) s = s + sL[ix(i, j)] * x[j];
+            for (int j = 1; j < i; ++j) s = FAST ? fma(sL[ix(i, j)], x[j], s) : s + sL[ix(i, j)] * x[j];
           }
-          x[i] = ((i == l ? 1.0 : 0.0) - s) / sL[ix(i, i)];
+          x[i] = FAST ? ((i == l ? 1.0 : 0.0) - s) * sL[ix(i, i)] : ((i == l ? 1.0 : 0.0) - s) / sL[ix(i, i)];
         }
 #pragma unroll
         for (int i = NX - 1; i >= 0; --i) {
@@ -540,9 +570,9 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
           if (i + 1 < NX) {
             s = sL[ix(i + 1, i)] * x[i + 1];
 #pragma unroll
-            for (int j = i + 2; j < NX; ++j) s = s + sL[ix(j, i)] * x[j];
+            for (int j = i + 2; j < NX; ++j) s = FAST ? fma(sL[ix(j, i)], x[j], s) : s + sL[ix(j, i)] * x[j];
           }
-          x[i] = (x[i] - s) / sL[ix(i, i)];
+          x[i] = FAST ? (x[i] - s) * sL[ix(i, i)] : (x[i] - s) / sL[ix(i, i)];
         }
         __syncwarp(gmask);  // everyone is done reading chi (sC) before it becomes X
 #pragma unroll
@@ -574,7 +604,7 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
       for (int i = 0; i < NX; ++i) {
         double a = (-sA[ix(i, 0)]) * sM1[ix(l, 0)];
 #pragma unroll
-        for (int m = 1; m < NX; ++m) a = a + (-sA[ix(i, m)]) * sM1[ix(l, m)];
+        for (int m = 1; m < NX; ++m) a = FAST ? fma(-sA[ix(i, m)], sM1[ix(l, m)], a) : a + (-sA[ix(i, m)]) * sM1[ix(l, m)];
         sC[ix(i, l)] = a;
       }
       __syncwarp(gmask);
@@ -582,7 +612,7 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
       for (int i = 0; i < NX; ++i) {
         double a = sC[ix(i, 0)] * sD[ix(0, l)];
 #pragma unroll
-        for (int m = 1; m < NX; ++m) a = a + sC[ix(i, m)] * sD[ix(m, l)];
+        for (int m = 1; m < NX; ++m) a = FAST ? fma(sC[ix(i, m)], sD[ix(m, l)], a) : a + sC[ix(i, m)] * sD[ix(m, l)];
         stage(t, i, l, a);
       }
       flush(Pu, t);
