@@ -512,3 +512,26 @@ def test_pcg_breakdown_all_kernels(D, nx, nu, T):
         assert isinstance(errs[0], D.BreakdownError) and errs[0].iteration == want_it, (mode, errs[0])
         assert errs[1] is None
         assert b.download(D._lib.F_PCG_ITERS)[1, 0] == want_ok[1]
+
+
+@pytest.mark.parametrize("nx,nu,T", [(8, 4, 30), (8, 4, 100), (8, 4, 113)])
+def test_fast_nx8_kernels_agree_bitwise(D, nx, nu, T, monkeypatch):
+    """The n_x = 8 single-CTA FAST kernels fold every sum in the same order:
+    pcg_kernel_h8r (-S in registers, the default) and pcg_kernel_h8f return
+    bit-identical iterates and counts."""
+    th = aq_thetas(nx, nu, T, 77, 5)
+    b = D.Batch(D.affine_quadratic(nx, nu, T), 5)
+    b.upload(D._lib.F_THETA, th)
+    b.upload(D._lib.F_Z, np.zeros((5, b.nz)))
+    b.linearize()
+    b.assemble_schur()
+    b.assemble_gamma()
+    got = {}
+    for variant in ("", "h8f"):
+        monkeypatch.setenv("DOCP_PCG_VARIANT", variant)
+        b.upload(D._lib.F_LAMBDA, np.zeros((5, b.nl)))
+        b.pcg_solve(D.PcgConfig(mode="fast"))
+        got[variant] = (b.download(D._lib.F_LAMBDA), b.download(D._lib.F_PCG_ITERS)[:, 0])
+    for variant in ("h8f",):
+        assert np.array_equal(got[variant][1], got[""][1]), variant
+        assert np.array_equal(got[variant][0], got[""][0]), variant
