@@ -42,15 +42,25 @@ struct AsmShared {
 /// Phase A of K1 (problem.hpp:202-257): one thread per stage task. Writes the
 /// QpData of problem p and the first-error ranks; returns (block-uniform)
 /// whether the Schur phases may run. Ends with a __syncthreads. NX, NU > 0
-/// fix the block sizes at compile time (same arithmetic).
+/// fix the block sizes at compile time (same arithmetic). `stage`, when
+/// given, is shared memory for nz + nth doubles: z and theta are first
+/// copied there with coalesced loads, so the per-stage tasks read on-chip
+/// copies instead of issuing dependent global loads.
 template <int NX = 0, int NU = 0>
-__device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schur, AsmShared& sh) {
+__device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schur, AsmShared& sh,
+                                double* stage = nullptr) {
   const Dims d = v.d;
   const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T, bsz = nx * nx;
   const Family fam = Family::from(v.prob);
   const int tid = threadIdx.x;
   const double* th = v.theta + static_cast<long>(p) * d.nth;
   const double* z = v.z + static_cast<long>(p) * d.nz;
+  if (stage) {  // made visible by the __syncthreads below
+    for (int e = tid; e < d.nz; e += blockDim.x) stage[e] = z[e];
+    for (int e = tid; e < d.nth; e += blockDim.x) stage[d.nz + e] = th[e];
+    z = stage;
+    th = stage + d.nz;
+  }
   double* qd = v.qd + static_cast<long>(p) * d.nb * nx;
   double* lq = v.lq + static_cast<long>(p) * d.nb * nx;
   double* q = v.q + static_cast<long>(p) * d.nb * nx;
@@ -435,9 +445,11 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
     __syncwarp(gmask);
   };
 
+  const bool stage_in = d.nz + d.nth <= NG * Lay::GBUF;
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
-    if (!phase_linearize<NX, NU>(v, p, eps_pd, do_schur, sh)) {
+    // z / theta staged in the group buffers (free until phase B) when they fit
+    if (!phase_linearize<NX, NU>(v, p, eps_pd, do_schur, sh, stage_in ? sm_asm : nullptr)) {
       __syncthreads();
       continue;
     }
