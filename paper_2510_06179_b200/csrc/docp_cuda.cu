@@ -138,7 +138,8 @@ template <int NX, int NU, int TH>
 int launch_assemble_th(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur,
                        bool fast) {
   constexpr int NG = TH / NX;
-  const size_t smem = static_cast<size_t>(NG) * AsmLayout<NX, NU>::GBUF * sizeof(double);
+  // NG group buffers + the two-block P_t hand-off between rounds
+  const size_t smem = (static_cast<size_t>(NG) * AsmLayout<NX, NU>::GBUF + 2 * AsmLayout<NX, NU>::P2) * sizeof(double);
   auto kern = fast ? assemble_kernel_t<NX, NU, TH, true> : assemble_kernel_t<NX, NU, TH, false>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;

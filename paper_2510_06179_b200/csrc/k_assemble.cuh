@@ -464,172 +464,197 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
     double* Pu = blk + d.p_sup;
     stage0_blocks(v, p);
 
-    // ---------------- phase B (schur.hpp:143-167)
-    for (int t = g; t < T; t += NG) {
-      const double* lqt = lq + t * NX;
-      const double* lqn = lq + (t + 1) * NX;
-      const double* lrt = lr + t * NU;
-      const double* At = v.A + a_off(d, p, t);
-      const double* Bt = v.Bm + b_off(d, p, t);
+    // Rounds of NG consecutive stages (group g takes stage t0 + g): phase B of
+    // every group, a CTA barrier, then phase C of every group with P_t read
+    // from the previous group's shared buffer (group 0: the previous round's
+    // hand-off in `carry`, or Q_0 at t = 0) and sub_t, P_{t+1} still on-chip.
+    double* carry = sm_asm + NG * Lay::GBUF;  // [2][P2]
+    for (int t0 = 0; t0 < T; t0 += NG) {
+      const int t = t0 + g;
+      bool ok = t < T;  // the stage exists and chi_t factorised
+      double dq = 0.0;
+      // ---------------- phase B (schur.hpp:143-167)
+      if (ok) {
+        const double* lqt = lq + t * NX;
+        const double* lqn = lq + (t + 1) * NX;
+        const double* lrt = lr + t * NU;
+        const double* At = v.A + a_off(d, p, t);
+        const double* Bt = v.Bm + b_off(d, p, t);
 #pragma unroll
-      for (int k = l; k < B2; k += NX) sA[ix(k % NX, k / NX)] = At[k];
+        for (int k = l; k < B2; k += NX) sA[ix(k % NX, k / NX)] = At[k];
 #pragma unroll
-      for (int k = l; k < NX * NU; k += NX) sB[ix(k % NX, k / NX)] = Bt[k];
-      __syncwarp(gmask);
-      // M1(k, l) = (A(l,k)/lq_k)/lq_k ; M2(k, l) = (B(l,k)/lr_k)/lr_k
-      double c3, dq;
-      if constexpr (FAST) {  // lane k scales column k of A (of B) by 1/q_k (1/r_k)
-        dq = __drcp_rn(qdp[t * NX + l]);
-        c3 = __drcp_rn(qdp[(t + 1) * NX + l]);
+        for (int k = l; k < NX * NU; k += NX) sB[ix(k % NX, k / NX)] = Bt[k];
+        __syncwarp(gmask);
+        // M1(k, l) = (A(l,k)/lq_k)/lq_k ; M2(k, l) = (B(l,k)/lr_k)/lr_k
+        double c3;
+        if constexpr (FAST) {  // lane k scales column k of A (of B) by 1/q_k (1/r_k)
+          dq = __drcp_rn(qdp[t * NX + l]);
+          c3 = __drcp_rn(qdp[(t + 1) * NX + l]);
 #pragma unroll
-        for (int j = 0; j < NX; ++j) sM1[ix(l, j)] = sA[ix(j, l)] * dq;
-        if (l < NU) {
-          const double ir = __drcp_rn(rdp[t * NU + l]);
+          for (int j = 0; j < NX; ++j) sM1[ix(l, j)] = sA[ix(j, l)] * dq;
+          if (l < NU) {
+            const double ir = __drcp_rn(rdp[t * NU + l]);
 #pragma unroll
-          for (int j = 0; j < NX; ++j) sM2[iu(l, j)] = sB[ix(j, l)] * ir;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < NX; ++k) sM1[ix(k, l)] = (sA[ix(l, k)] / lqt[k]) / lqt[k];
-#pragma unroll
-        for (int k = 0; k < NU; ++k) sM2[iu(k, l)] = (sB[ix(l, k)] / lrt[k]) / lrt[k];
-        c3 = (1.0 / lqn[l]) / lqn[l];
-        dq = (1.0 / lqt[l]) / lqt[l];
-      }
-      __syncwarp(gmask);
-      // column l of chi = A M1 + B M2 + A+ Q+^-1 A+'  and of phi_t = A Q_t^-1
-#pragma unroll
-      for (int i = 0; i < NX; ++i) {
-        double a = sA[ix(i, 0)] * sM1[ix(0, l)];
-        double b = sB[ix(i, 0)] * sM2[iu(0, l)];
-        if constexpr (FAST) {
-#pragma unroll
-          for (int m = 1; m < NX; ++m) a = fma(sA[ix(i, m)], sM1[ix(m, l)], a);
-#pragma unroll
-          for (int m = 1; m < NU; ++m) b = fma(sB[ix(i, m)], sM2[iu(m, l)], b);
+            for (int j = 0; j < NX; ++j) sM2[iu(l, j)] = sB[ix(j, l)] * ir;
+          }
         } else {
 #pragma unroll
-          for (int m = 1; m < NX; ++m) a = a + sA[ix(i, m)] * sM1[ix(m, l)];
+            for (int k = 0; k < NX; ++k) sM1[ix(k, l)] = (sA[ix(l, k)] / lqt[k]) / lqt[k];
 #pragma unroll
-          for (int m = 1; m < NU; ++m) b = b + sB[ix(i, m)] * sM2[iu(m, l)];
-        }
-        sC[ix(i, l)] = (a + b) + (i == l ? c3 : 0.0);
-      }
-      __syncwarp(gmask);  // B_t / M2 are dead: sO takes their place
-#pragma unroll
-      for (int i = 0; i < NX; ++i) stage(t, i, l, sA[ix(i, l)] * dq);
-      flush(Ss, t);
-#pragma unroll
-      for (int i = 0; i < NX; ++i) {
-        const double dv = 0.5 * (sC[ix(i, l)] + sC[ix(l, i)]);
-        sD[ix(i, l)] = dv;
-        stage(t + 1, i, l, dv);
-        sM1[ix(i, l)] = 0.0;  // becomes L
-      }
-      flush(Sd, t + 1);
-      // Cholesky of chi_t (eigen_lite LLT): lane l computes row l
-      double* sL = sM1;
-      bool failed = false;
-#pragma unroll
-      for (int k = 0; k < NX; ++k) {
-        double s = 0.0;
-        if (k > 0) {
-          s = sL[ix(k, 0)] * sL[ix(k, 0)];
-#pragma unroll
-          for (int j = 1; j < k; ++j) s = FAST ? fma(sL[ix(k, j)], sL[ix(k, j)], s) : s + sL[ix(k, j)] * sL[ix(k, j)];
-        }
-        const double piv = sD[ix(k, k)] - s;
-        if (piv <= 0.0) {
-          failed = true;
-          break;
-        }
-        // FAST: the factor's diagonal holds 1/l_kk (only the solves read it)
-        const double lk = FAST ? rsqrt(piv) : sqrt(piv);
-        if (l == k) sL[ix(k, k)] = lk;
-        if (l > k) {
-          double tt = 0.0;
-          if (k > 0) {
-            tt = sL[ix(l, 0)] * sL[ix(k, 0)];
-#pragma unroll
-            for (int j = 1; j < k; ++j) tt = FAST ? fma(sL[ix(l, j)], sL[ix(k, j)], tt) : tt + sL[ix(l, j)] * sL[ix(k, j)];
+            for (int k = 0; k < NU; ++k) sM2[iu(k, l)] = (sB[ix(l, k)] / lrt[k]) / lrt[k];
+            c3 = (1.0 / lqn[l]) / lqn[l];
+            dq = (1.0 / lqt[l]) / lqt[l];
           }
-          sL[ix(l, k)] = FAST ? (sD[ix(l, k)] - tt) * lk : (sD[ix(l, k)] - tt) / lk;
+          __syncwarp(gmask);
+          // column l of chi = A M1 + B M2 + A+ Q+^-1 A+'  and of phi_t = A Q_t^-1
+#pragma unroll
+          for (int i = 0; i < NX; ++i) {
+            double a = sA[ix(i, 0)] * sM1[ix(0, l)];
+            double b = sB[ix(i, 0)] * sM2[iu(0, l)];
+            if constexpr (FAST) {
+#pragma unroll
+              for (int m = 1; m < NX; ++m) a = fma(sA[ix(i, m)], sM1[ix(m, l)], a);
+#pragma unroll
+              for (int m = 1; m < NU; ++m) b = fma(sB[ix(i, m)], sM2[iu(m, l)], b);
+            } else {
+#pragma unroll
+              for (int m = 1; m < NX; ++m) a = a + sA[ix(i, m)] * sM1[ix(m, l)];
+#pragma unroll
+              for (int m = 1; m < NU; ++m) b = b + sB[ix(i, m)] * sM2[iu(m, l)];
+            }
+            sC[ix(i, l)] = (a + b) + (i == l ? c3 : 0.0);
+          }
+          __syncwarp(gmask);  // B_t / M2 are dead: sO takes their place
+#pragma unroll
+          for (int i = 0; i < NX; ++i) stage(t, i, l, sA[ix(i, l)] * dq);
+          flush(Ss, t);
+#pragma unroll
+          for (int i = 0; i < NX; ++i) {
+            const double dv = 0.5 * (sC[ix(i, l)] + sC[ix(l, i)]);
+            sD[ix(i, l)] = dv;
+            stage(t + 1, i, l, dv);
+            sM1[ix(i, l)] = 0.0;  // becomes L
+          }
+          flush(Sd, t + 1);
+          // Cholesky of chi_t (eigen_lite LLT): lane l computes row l
+          double* sL = sM1;
+          bool failed = false;
+#pragma unroll
+          for (int k = 0; k < NX; ++k) {
+            double s = 0.0;
+            if (k > 0) {
+              s = sL[ix(k, 0)] * sL[ix(k, 0)];
+#pragma unroll
+              for (int j = 1; j < k; ++j) s = FAST ? fma(sL[ix(k, j)], sL[ix(k, j)], s) : s + sL[ix(k, j)] * sL[ix(k, j)];
+            }
+            const double piv = sD[ix(k, k)] - s;
+            if (piv <= 0.0) {
+              failed = true;
+              break;
+            }
+            // FAST: the factor's diagonal holds 1/l_kk (only the solves read it)
+            const double lk = FAST ? rsqrt(piv) : sqrt(piv);
+            if (l == k) sL[ix(k, k)] = lk;
+            if (l > k) {
+              double tt = 0.0;
+              if (k > 0) {
+                tt = sL[ix(l, 0)] * sL[ix(k, 0)];
+#pragma unroll
+                for (int j = 1; j < k; ++j) tt = FAST ? fma(sL[ix(l, j)], sL[ix(k, j)], tt) : tt + sL[ix(l, j)] * sL[ix(k, j)];
+              }
+              sL[ix(l, k)] = FAST ? (sD[ix(l, k)] - tt) * lk : (sD[ix(l, k)] - tt) / lk;
+            }
+            __syncwarp(gmask);
+          }
+          if (failed) {
+            if (l == 0) atomicMin(&sh.rank_chi, t);
+            __syncwarp(gmask);
+            ok = false;
+          } else {
+          // chi_t^-1 = chol.solve(I): lane l solves column l
+          double* sX = sC;
+          {
+            double x[NX];
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+              double s = 0.0;
+              if (i > 0) {
+                s = sL[ix(i, 0)] * x[0];
+#pragma unroll
+                for (int j = 1; j < i; ++j) s = FAST ? fma(sL[ix(i, j)], x[j], s) : s + sL[ix(i, j)] * x[j];
+              }
+              x[i] = FAST ? ((i == l ? 1.0 : 0.0) - s) * sL[ix(i, i)] : ((i == l ? 1.0 : 0.0) - s) / sL[ix(i, i)];
+            }
+#pragma unroll
+            for (int i = NX - 1; i >= 0; --i) {
+              double s = 0.0;
+              if (i + 1 < NX) {
+                s = sL[ix(i + 1, i)] * x[i + 1];
+#pragma unroll
+                for (int j = i + 2; j < NX; ++j) s = FAST ? fma(sL[ix(j, i)], x[j], s) : s + sL[ix(j, i)] * x[j];
+              }
+              x[i] = FAST ? (x[i] - s) * sL[ix(i, i)] : (x[i] - s) / sL[ix(i, i)];
+            }
+            __syncwarp(gmask);  // everyone is done reading chi (sC) before it becomes X
+#pragma unroll
+            for (int i = 0; i < NX; ++i) sX[ix(i, l)] = x[i];
+          }
+          __syncwarp(gmask);
+#pragma unroll
+          for (int i = 0; i < NX; ++i) {
+            const double pv = 0.5 * (sX[ix(i, l)] + sX[ix(l, i)]);
+            stage(t + 1, i, l, pv);
+            sD[ix(i, l)] = pv;  // P_{t+1} for phase C (sym(chi) is dead after the factorisation)
+          }
+          flush(Pd, t + 1);
+#pragma unroll
+          for (int i = 0; i < NX; ++i) sM1[ix(i, l)] = sA[ix(i, l)] * dq;  // sub_t (= the Ss_t block); L is dead
+        }  // chi_t factorised
+      }  // stage exists
+      __syncthreads();
+
+      // ---------------- phase C: stair off-diagonal (-D_t phi_t') D_{t+1} (schur.hpp:169-179)
+      if (ok) {
+        const double* Pt;
+        if (g > 0) {
+          Pt = sm_asm + static_cast<long>(g - 1) * Lay::GBUF + 3 * Lay::P2;  // previous group's P_t
+        } else if (t > 0) {
+          Pt = carry + ((t0 / NG - 1) & 1) * Lay::P2;
+        } else {  // P_0 = Q_0 (stage0_blocks)
+          const double* qd0 = v.qd + static_cast<long>(p) * d.nb * NX;
+#pragma unroll
+          for (int i = 0; i < NX; ++i) sA[ix(i, l)] = i == l ? qd0[l] : 0.0;
+          __syncwarp(gmask);
+          Pt = sA;
         }
-        __syncwarp(gmask);
-      }
-      if (failed) {
-        if (l == 0) atomicMin(&sh.rank_chi, t);
-        __syncwarp(gmask);
-        continue;
-      }
-      // chi_t^-1 = chol.solve(I): lane l solves column l
-      double* sX = sC;
-      {
-        double x[NX];
+        // T1(i, l) = sum_m (-P_t(i,m)) sub_t(l,m)
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
-          double s = 0.0;
-          if (i > 0) {
-            s = sL[ix(i, 0)] * x[0];
+          double a = (-Pt[ix(i, 0)]) * sM1[ix(l, 0)];
 #pragma unroll
-            for (int j = 1; j < i; ++j) s = FAST ? fma(sL[ix(i, j)], x[j], s) : s + sL[ix(i, j)] * x[j];
-          }
-          x[i] = FAST ? ((i == l ? 1.0 : 0.0) - s) * sL[ix(i, i)] : ((i == l ? 1.0 : 0.0) - s) / sL[ix(i, i)];
+          for (int m = 1; m < NX; ++m) a = FAST ? fma(-Pt[ix(i, m)], sM1[ix(l, m)], a) : a + (-Pt[ix(i, m)]) * sM1[ix(l, m)];
+          sC[ix(i, l)] = a;
         }
+        __syncwarp(gmask);
 #pragma unroll
-        for (int i = NX - 1; i >= 0; --i) {
-          double s = 0.0;
-          if (i + 1 < NX) {
-            s = sL[ix(i + 1, i)] * x[i + 1];
+        for (int i = 0; i < NX; ++i) {
+          double a = sC[ix(i, 0)] * sD[ix(0, l)];
 #pragma unroll
-            for (int j = i + 2; j < NX; ++j) s = FAST ? fma(sL[ix(j, i)], x[j], s) : s + sL[ix(j, i)] * x[j];
-          }
-          x[i] = FAST ? (x[i] - s) * sL[ix(i, i)] : (x[i] - s) / sL[ix(i, i)];
+          for (int m = 1; m < NX; ++m) a = FAST ? fma(sC[ix(i, m)], sD[ix(m, l)], a) : a + sC[ix(i, m)] * sD[ix(m, l)];
+          stage(t, i, l, a);
         }
-        __syncwarp(gmask);  // everyone is done reading chi (sC) before it becomes X
+        flush(Pu, t);
+        if (g == NG - 1) {  // hand P_{t+1} to group 0 of the next round
 #pragma unroll
-        for (int i = 0; i < NX; ++i) sX[ix(i, l)] = x[i];
+          for (int i = 0; i < NX; ++i) carry[((t0 / NG) & 1) * Lay::P2 + ix(i, l)] = sD[ix(i, l)];
+        }
       }
-      __syncwarp(gmask);
-#pragma unroll
-      for (int i = 0; i < NX; ++i) stage(t + 1, i, l, 0.5 * (sX[ix(i, l)] + sX[ix(l, i)]));
-      flush(Pd, t + 1);
+      __syncthreads();
     }
-    __syncthreads();
     if (sh.rank_chi != kNoError) {
       if (tid == 0) set_status(v.status + p, DOCP_NUMERICAL, DOCP_AT_CHOL_CHI, sh.rank_chi);
-      __syncthreads();
-      continue;
     }
-
-    // ---------------- phase C: stair off-diagonal (-D_t phi_t') D_{t+1} (schur.hpp:169-179)
-    for (int t = g; t < T; t += NG) {
-#pragma unroll
-      for (int i = 0; i < NX; ++i) {
-        sA[ix(i, l)] = blk_load(Pd, NX, t, i, l);
-        sM1[ix(i, l)] = blk_load(Ss, NX, t, i, l);
-        sD[ix(i, l)] = blk_load(Pd, NX, t + 1, i, l);
-      }
-      __syncwarp(gmask);
-      // T1(i, l) = sum_m (-P_t(i,m)) sub_t(l,m)
-#pragma unroll
-      for (int i = 0; i < NX; ++i) {
-        double a = (-sA[ix(i, 0)]) * sM1[ix(l, 0)];
-#pragma unroll
-        for (int m = 1; m < NX; ++m) a = FAST ? fma(-sA[ix(i, m)], sM1[ix(l, m)], a) : a + (-sA[ix(i, m)]) * sM1[ix(l, m)];
-        sC[ix(i, l)] = a;
-      }
-      __syncwarp(gmask);
-#pragma unroll
-      for (int i = 0; i < NX; ++i) {
-        double a = sC[ix(i, 0)] * sD[ix(0, l)];
-#pragma unroll
-        for (int m = 1; m < NX; ++m) a = FAST ? fma(sC[ix(i, m)], sD[ix(m, l)], a) : a + sC[ix(i, m)] * sD[ix(m, l)];
-        stage(t, i, l, a);
-      }
-      flush(Pu, t);
-    }
-    __syncthreads();
+    __syncthreads();  // sh is re-initialised by the next problem
   }
 }
 
