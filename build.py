@@ -5,6 +5,7 @@
   oracle/_build/libdocp_port.so               C restatement (test checker)
   oracle/_ref/*                               reference headers + eigen_lite
                                               (only where /root/reference exists)
+  paper_2510_06179_b200/lib/docp_gpu          CLI (`solve`, `grad-check`) over the C ABI
   tests/cpp/_bin/test_dropin                  C++ drop-in tests (docp_gpu.hpp vs the
                                               reference headers; same condition)
 """
@@ -63,6 +64,20 @@ def build_cuda(force=False, verbose=False):
         print("built", LIB)
 
 
+CLI_SRC = os.path.join(ROOT, "paper_2510_06179_b200", "cli")
+CLI = os.path.join(os.path.dirname(LIB), "docp_gpu")
+
+
+def build_cli(force=False):
+    """The docp_main.cpp `solve` / `grad-check` front-end on the GPU path."""
+    sources = [os.path.join(CLI_SRC, f) for f in os.listdir(CLI_SRC)] + [LIB, os.path.join(ROOT, "include", "docp_cuda.h")]
+    if not force and not _stale(CLI, sources):
+        return
+    subprocess.run(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    "-o", CLI, os.path.join(CLI_SRC, "docp_gpu_main.cpp"), "-L", os.path.dirname(LIB),
+                    "-ldocp_cuda", "-Wl,-rpath,$ORIGIN"], check=True)
+
+
 def build_oracle():
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "port"], check=True)
     if os.path.isdir("/root/reference/proj/include"):
@@ -72,6 +87,7 @@ def build_oracle():
 
 def main():
     build_cuda(force="--force" in sys.argv, verbose=True)
+    build_cli(force="--force" in sys.argv)
     build_oracle()
 
 
