@@ -274,8 +274,9 @@ def run_ours(args):
     cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode=args.mode))
     den = float(B * world)
 
-    def epoch():
-        b.il_epoch(cfg, w.data_ptr(), 0, NX, demos.data_ptr(), den, out.data_ptr(), out.data_ptr() + 8)
+    def epoch(demo_buf=None):
+        dptr = (demos if demo_buf is None else demo_buf).data_ptr()
+        b.il_epoch(cfg, w.data_ptr(), 0, NX, dptr, den, out.data_ptr(), out.data_ptr() + 8)
         tot = fixed_order_allreduce(out) if world > 1 else out
         w.sub_(LR * tot[1:])
         return tot
@@ -355,20 +356,39 @@ def run_ours(args):
             traffic = json.load(fh).get("dram_bytes_per_launch")
     solves = max(1, prof["pcg_solves"])
 
-    # e2e: the same epochs through the C ABI with host buffers (pinned), copies timed
+    # e2e: the same epochs through the public API with HOST inputs: every
+    # step copies its theta and demonstrations from pinned host memory and
+    # reads its loss + gradient back. The copy of step k+1's inputs runs on a
+    # second stream while step k computes (double-buffered device copies, as
+    # a data loader prefetches); the first step's copy is exposed.
     restore(state0)
     th_pin = torch.tensor(thetas).pin_memory()
     demos_pin = torch.tensor(demos_host).pin_memory()
     w_pin = w.cpu().pin_memory()
     res_pin = torch.zeros(1 + NX, dtype=torch.float64).pin_memory()
+    copy_stream = torch.cuda.Stream(dev)
+    th_dev = [torch.empty(th_pin.shape, dtype=torch.float64, device=dev) for _ in range(2)]
+    demos_dev = [torch.empty(demos_pin.shape, dtype=torch.float64, device=dev) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+
+    def prefetch(k):  # host -> device copy of step k's inputs into slot k % 2
+        with torch.cuda.stream(copy_stream):
+            th_dev[k % 2].copy_(th_pin, non_blocking=True)
+            demos_dev[k % 2].copy_(demos_pin, non_blocking=True)
+            ready[k % 2].record(copy_stream)
+
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        b.upload(L.F_THETA, th_pin.numpy())          # docp_batch_upload (host -> device)
-        demos.copy_(demos_pin, non_blocking=True)
+    copy_stream.wait_event(e0)
+    prefetch(0)
+    for k in range(args.steps):
+        stream.wait_event(ready[k % 2])
+        b.upload(L.F_THETA, th_dev[k % 2])           # docp_batch_upload (device copy of the step's theta)
         w.copy_(w_pin, non_blocking=True)
-        tot = epoch()
+        if k + 1 < args.steps:
+            prefetch(k + 1)   # slot (k+1) % 2 was last read by step k-1, finished (synchronized) below
+        tot = epoch(demos_dev[k % 2])
         res_pin.copy_(tot, non_blocking=True)
         stream.synchronize()
         w_pin = (w_pin - LR * res_pin[1:]).contiguous()

@@ -272,6 +272,14 @@ class Batch:
         _raise_call(L.lib().docp_batch_sync(self.h))
 
     def upload(self, f: int, a):
+        """Host array (synchronous copy) or a CUDA tensor (device-to-device
+        copy ordered on the batch's stream)."""
+        if getattr(a, "is_cuda", False):
+            _, n = self.field_ptr(f)
+            if not a.is_contiguous() or a.numel() * a.element_size() != n:
+                raise DimensionError(f"field {f}: expected {n} contiguous bytes")
+            _raise_call(L.lib().docp_batch_upload(self.h, f, C.c_void_p(a.data_ptr()), 1))
+            return
         dtype = np.float64 if f in _FLOAT_FIELDS else np.int32
         arr = np.ascontiguousarray(a, dtype=dtype)
         _, n = self.field_ptr(f)

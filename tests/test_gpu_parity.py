@@ -514,7 +514,7 @@ def test_pcg_breakdown_all_kernels(D, nx, nu, T):
         assert b.download(D._lib.F_PCG_ITERS)[1, 0] == want_ok[1]
 
 
-@pytest.mark.parametrize("nx,nu,T", [(8, 4, 30), (8, 4, 100), (8, 4, 113)])
+@pytest.mark.parametrize("nx,nu,T", [(8, 4, 1), (8, 4, 2), (8, 4, 30), (8, 4, 100), (8, 4, 113)])
 def test_fast_nx8_kernels_agree_bitwise(D, nx, nu, T, monkeypatch):
     """The n_x = 8 single-CTA FAST kernels fold every sum in the same order:
     pcg_kernel_h8r (-S in registers, the default) and pcg_kernel_h8f return
