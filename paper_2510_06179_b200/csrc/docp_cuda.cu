@@ -180,21 +180,50 @@ int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint
   return DOCP_OK;
 }
 
-int launch_gamma(docp_batch* b, const int* list, const int* count, int n_hint, int rhs) {
-  ProfScope ps(b, DOCP_PROF_GAMMA);
-  const size_t smem = (static_cast<size_t>(b->d.nb) * b->d.nx + static_cast<size_t>(b->d.T) * b->d.nu) * 8;
-  CUDA_TRY(cudaFuncSetAttribute(gamma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  gamma_kernel<<<std::max(1, std::min(n_hint, b->num_sms * 8)), 128, smem, b->stream>>>(b->v, list, count, rhs);
+/// One CTA per problem (grid-stride over the work list), the grid sized to
+/// the resident CTAs of the whole GPU.
+template <class K, class... A>
+int launch_per_problem(docp_batch* b, K kern, int threads, size_t smem, int n_hint, A... args) {
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "kernel does not fit on an SM (smem %zu)", smem);
+  kern<<<std::max(1, std::min(n_hint, per_sm * b->num_sms)), threads, smem, b->stream>>>(b->v, args...);
   LAUNCH_CHECK();
   return DOCP_OK;
 }
 
+/// Compile-time block sizes for the shipped configurations, runtime otherwise.
+#define DOCP_DISPATCH_NXNU(nx, nu, CALL)                        \
+  do {                                                          \
+    if ((nx) == 8 && (nu) == 4) { constexpr int NX = 8, NU = 4; CALL; } \
+    if ((nx) == 8 && (nu) == 2) { constexpr int NX = 8, NU = 2; CALL; } \
+    if ((nx) == 4 && (nu) == 1) { constexpr int NX = 4, NU = 1; CALL; } \
+    if ((nx) == 4 && (nu) == 2) { constexpr int NX = 4, NU = 2; CALL; } \
+    { constexpr int NX = 0, NU = 0; CALL; }                     \
+  } while (0)
+
+int launch_gamma(docp_batch* b, const int* list, const int* count, int n_hint, int rhs) {
+  ProfScope ps(b, DOCP_PROF_GAMMA);
+  const size_t smem = (static_cast<size_t>(b->d.nb) * b->d.nx + static_cast<size_t>(b->d.T) * b->d.nu) * 8;
+  DOCP_DISPATCH_NXNU(b->d.nx, b->d.nu,
+                     return launch_per_problem(b, gamma_kernel<NX, NU>, 128, smem, n_hint, list, count, rhs));
+}
+
 int launch_recover(docp_batch* b, const int* list, const int* count, int n_hint, const double* lam, int rhs) {
   ProfScope ps(b, DOCP_PROF_RECOVER);
-  recover_kernel<<<grid_for(static_cast<long>(n_hint) * b->d.nz, 256, b->num_sms * 16), 256, 0, b->stream>>>(
-      b->v, list, count, lam, rhs);
-  LAUNCH_CHECK();
-  return DOCP_OK;
+  const size_t smem = static_cast<size_t>(b->d.nl) * 8;
+  DOCP_DISPATCH_NXNU(b->d.nx, b->d.nu,
+                     return launch_per_problem(b, recover_kernel<NX, NU>, 128, smem, n_hint, list, count, lam, rhs));
+}
+
+int launch_vjp(docp_batch* b, const int* list, const int* count, int n_hint) {
+  ProfScope ps(b, DOCP_PROF_VJP);
+  size_t smem = (2 * static_cast<size_t>(b->d.nz) + 2 * static_cast<size_t>(b->d.nl)) * 8;
+  const int staged = smem <= 96 * 1024;  // long horizons read the vectors in place
+  if (!staged) smem = 0;
+  DOCP_DISPATCH_NXNU(b->d.nx, b->d.nu,
+                     return launch_per_problem(b, vjp_kernel<NX, NU>, 128, smem, n_hint, list, count, staged));
 }
 
 size_t pcg_smem(const Dims& d, bool resident) {
@@ -713,11 +742,7 @@ int docp_backward_vjp(docp_batch* b, const docp_pcg_config* cfg) {  // backward.
   if ((rc = launch_gamma(b, list, cnt, b->B, DOCP_RHS_ADJOINT))) return rc;
   if ((rc = launch_pcg(b, *cfg, list, cnt, b->B, b->v.lt))) return rc;
   if ((rc = launch_recover(b, list, cnt, b->B, b->v.lt, DOCP_RHS_ADJOINT))) return rc;
-  ProfScope ps(b, DOCP_PROF_VJP);
-  vjp_kernel<<<grid_for(static_cast<long>(b->B) * b->d.nth, 128, b->num_sms * 16), 128, 0, b->stream>>>(b->v, list,
-                                                                                                        cnt);
-  LAUNCH_CHECK();
-  return DOCP_OK;
+  return launch_vjp(b, list, cnt, b->B);
 }
 
 // ---------------------------------------------------------------- rollouts (batch.hpp:172-258)

@@ -664,32 +664,39 @@ __device__ inline double diag_solve(double b, double l) { return (b / l) / l; }
 /// GAMMA <- -(d + H G^-1 b) (schur.hpp:187-211), one CTA per problem: the
 /// block solves Q_t^-1 b_x, R_t^-1 b_u are formed once per entry into SMEM
 /// (two divisions each, as the reference's LLT solves), then every output row
-/// folds them in the reference order.
+/// folds them in the reference order. NX, NU > 0 fix the block sizes at
+/// compile time (the index arithmetic folds; same floating-point operations).
 /// rhs FORWARD: b = flat_b, d = flat_d; ADJOINT: b = -LOSS_GRAD_Z, d = 0.
-__global__ void gamma_kernel(View v, const int* __restrict__ work, const int* __restrict__ n_work, int rhs) {
+template <int NX = 0, int NU = 0>
+__global__ void __launch_bounds__(128) gamma_kernel(View v, const int* __restrict__ work,
+                                                    const int* __restrict__ n_work, int rhs) {
   extern __shared__ double sm_gam[];
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, T = d.T;
+  const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T;
+  const int nb = T + 1, nl = nb * nx, nz = nl + T * nu, sz = nx + nu;
   double* sq = sm_gam;              // [T+1][nx]
-  double* su = sm_gam + d.nb * nx;  // [T][nu]
+  double* su = sm_gam + nb * nx;    // [T][nu]
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
-    const double* lq = v.lq + static_cast<long>(p) * d.nb * nx;
+    const double* lq = v.lq + static_cast<long>(p) * nb * nx;
     const double* lr = v.lr + static_cast<long>(p) * T * nu;
-    const double* lg = v.lgz + static_cast<long>(p) * d.nz;
-    for (int e = threadIdx.x; e < d.nb * nx; e += blockDim.x) {
-      const int t = e / nx, k = e % nx;
-      const double b = rhs == DOCP_RHS_FORWARD ? v.q[static_cast<long>(p) * d.nb * nx + e] : -lg[xoff(d, t) + k];
+    const double* lg = v.lgz + static_cast<long>(p) * nz;
+    const double* qp = v.q + static_cast<long>(p) * nb * nx;
+    const double* rp = v.r + static_cast<long>(p) * T * nu;
+    for (int e = threadIdx.x; e < nb * nx; e += blockDim.x) {
+      const int t = e / nx, k = e - t * nx;
+      const double b = rhs == DOCP_RHS_FORWARD ? qp[e] : -lg[t * sz + k];
       sq[e] = diag_solve(b, lq[e]);
     }
     for (int e = threadIdx.x; e < T * nu; e += blockDim.x) {
-      const int t = e / nu, k = e % nu;
-      const double b = rhs == DOCP_RHS_FORWARD ? v.r[static_cast<long>(p) * T * nu + e] : -lg[uoff(d, t) + k];
+      const int t = e / nu, k = e - t * nu;
+      const double b = rhs == DOCP_RHS_FORWARD ? rp[e] : -lg[t * sz + nx + k];
       su[e] = diag_solve(b, lr[e]);
     }
     __syncthreads();
-    for (int row = threadIdx.x; row < d.nl; row += blockDim.x) {
-      const int blk = row / nx, i = row % nx;
+    const double* Cp = v.C + static_cast<long>(p) * T * nx;
+    for (int row = threadIdx.x; row < nl; row += blockDim.x) {
+      const int blk = row / nx, i = row - blk * nx;
       double out;
       if (blk == 0) {
         const double dd = rhs == DOCP_RHS_FORWARD ? v.xs[static_cast<long>(p) * nx + i] : 0.0;
@@ -701,56 +708,70 @@ __global__ void gamma_kernel(View v, const int* __restrict__ work, const int* __
         const double* s0 = sq + t * nx;
         const double* s1 = su + t * nu;
         double a = At[i] * s0[0];
+#pragma unroll
         for (int k = 1; k < nx; ++k) a = a + At[i + k * nx] * s0[k];
         double b = Bt[i] * s1[0];
+#pragma unroll
         for (int k = 1; k < nu; ++k) b = b + Bt[i + k * nx] * s1[k];
         const double c = sq[(t + 1) * nx + i];
-        const double dd = rhs == DOCP_RHS_FORWARD ? v.C[(static_cast<long>(p) * T + t) * nx + i] : 0.0;
+        const double dd = rhs == DOCP_RHS_FORWARD ? Cp[t * nx + i] : 0.0;
         out = dd + ((a + b) + c);
       }
-      v.gamma[static_cast<long>(p) * d.nl + row] = -out;
+      v.gamma[static_cast<long>(p) * nl + row] = -out;
     }
     __syncthreads();
   }
 }
 
-/// Z_QP <- recover_primal(lambda, b) (sqp.hpp:62-89), one thread per primal entry.
-__global__ void recover_kernel(View v, const int* __restrict__ work, const int* __restrict__ n_work,
-                               const double* __restrict__ lam_all, int rhs) {
+/// Z_QP <- recover_primal(lambda, b) (sqp.hpp:62-89), one CTA per problem:
+/// the problem's multipliers are staged in shared memory with coalesced
+/// loads, then one thread per primal entry folds in the reference order.
+template <int NX = 0, int NU = 0>
+__global__ void __launch_bounds__(128) recover_kernel(View v, const int* __restrict__ work,
+                                                      const int* __restrict__ n_work,
+                                                      const double* __restrict__ lam_all, int rhs) {
+  extern __shared__ double sm_rec[];  // [n_lambda]
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, T = d.T;
-  const long total = static_cast<long>(*n_work) * d.nz;
-  for (long g = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; g < total;
-       g += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int p = work[g / d.nz];
-    const int e = static_cast<int>(g % d.nz);
-    const int t = e / (nx + nu), c = e % (nx + nu);
-    const double* lam = lam_all + static_cast<long>(p) * d.nl;
-    const double* lg = v.lgz + static_cast<long>(p) * d.nz;
-    double rhs_v = rhs == DOCP_RHS_FORWARD ? 0.0 : -lg[e];
-    double out;
-    if (c < nx) {  // x_t,c = -Q_t^-1 (b + A+_{t-1}' lam_t + A_t' lam_{t+1})
-      const int i = c;
-      if (rhs == DOCP_RHS_FORWARD) rhs_v = v.q[(static_cast<long>(p) * d.nb + t) * nx + i];
-      rhs_v = rhs_v + lam[t * nx + i];
-      if (t < T) {
-        const double* At = v.A + a_off(d, p, t);
+  const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T;
+  const int nb = T + 1, nl = nb * nx, nz = nl + T * nu, sz = nx + nu;
+  for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
+    const int p = work[w];
+    const double* lamg = lam_all + static_cast<long>(p) * nl;
+    for (int e = threadIdx.x; e < nl; e += blockDim.x) sm_rec[e] = lamg[e];
+    __syncthreads();
+    const double* lam = sm_rec;
+    const double* lg = v.lgz + static_cast<long>(p) * nz;
+    double* zq = v.zqp + static_cast<long>(p) * nz;
+    for (int e = threadIdx.x; e < nz; e += blockDim.x) {
+      const int t = e / sz, c = e - t * sz;
+      double rhs_v = rhs == DOCP_RHS_FORWARD ? 0.0 : -lg[e];
+      double out;
+      if (c < nx) {  // x_t,c = -Q_t^-1 (b + A+_{t-1}' lam_t + A_t' lam_{t+1})
+        const int i = c;
+        if (rhs == DOCP_RHS_FORWARD) rhs_v = v.q[(static_cast<long>(p) * nb + t) * nx + i];
+        rhs_v = rhs_v + lam[t * nx + i];
+        if (t < T) {
+          const double* At = v.A + a_off(d, p, t);
+          const double* l1 = lam + (t + 1) * nx;
+          double a = At[i * nx] * l1[0];
+#pragma unroll
+          for (int k = 1; k < nx; ++k) a = a + At[k + i * nx] * l1[k];
+          rhs_v = rhs_v + a;
+        }
+        out = -diag_solve(rhs_v, v.lq[(static_cast<long>(p) * nb + t) * nx + i]);
+      } else {  // u_t,i = -R_t^-1 (b + B_t' lam_{t+1})
+        const int i = c - nx;
+        if (rhs == DOCP_RHS_FORWARD) rhs_v = v.r[(static_cast<long>(p) * T + t) * nu + i];
+        const double* Bt = v.Bm + b_off(d, p, t);
         const double* l1 = lam + (t + 1) * nx;
-        double a = At[i * nx] * l1[0];
-        for (int k = 1; k < nx; ++k) a = a + At[k + i * nx] * l1[k];
-        rhs_v = rhs_v + a;
+        double a = Bt[i * nx] * l1[0];
+#pragma unroll
+        for (int k = 1; k < nx; ++k) a = a + Bt[k + i * nx] * l1[k];
+        out = -diag_solve(rhs_v + a, v.lr[(static_cast<long>(p) * T + t) * nu + i]);
       }
-      out = -diag_solve(rhs_v, v.lq[(static_cast<long>(p) * d.nb + t) * nx + i]);
-    } else {  // u_t,i = -R_t^-1 (b + B_t' lam_{t+1})
-      const int i = c - nx;
-      if (rhs == DOCP_RHS_FORWARD) rhs_v = v.r[(static_cast<long>(p) * T + t) * nu + i];
-      const double* Bt = v.Bm + b_off(d, p, t);
-      const double* l1 = lam + (t + 1) * nx;
-      double a = Bt[i * nx] * l1[0];
-      for (int k = 1; k < nx; ++k) a = a + Bt[k + i * nx] * l1[k];
-      out = -diag_solve(rhs_v + a, v.lr[(static_cast<long>(p) * T + t) * nu + i]);
+      zq[e] = out;
     }
-    v.zqp[static_cast<long>(p) * d.nz + e] = out;
+    __syncthreads();
   }
 }
 

@@ -366,54 +366,72 @@ __global__ void __launch_bounds__(kKktThreads) kkt_kernel(View v, const int* __r
   }
 }
 
-/// K4 epilogue: GRAD_THETA = theta_vjp(z, lambda, z~ = Z_QP, lambda~), one
-/// thread per theta entry folding over t in the reference's order.
-__global__ void vjp_kernel(View v, const int* __restrict__ work, const int* __restrict__ n_work) {
+/// K4 epilogue: GRAD_THETA = theta_vjp(z, lambda, z~ = Z_QP, lambda~)
+/// (affine_quadratic.hpp:82-117, quadratic_cost.hpp:24-45). One CTA per
+/// problem: z, z~, lambda and lambda~ are staged in shared memory with
+/// coalesced loads (when they fit: `staged`), then one thread per theta
+/// entry folds over t in the reference's order. NX, NU > 0 fix the sizes at
+/// compile time.
+template <int NX = 0, int NU = 0>
+__global__ void __launch_bounds__(128) vjp_kernel(View v, const int* __restrict__ work,
+                                                  const int* __restrict__ n_work, int staged) {
+  extern __shared__ double sm_vjp[];  // z [nz] | z~ [nz] | lambda [nl] | lambda~ [nl]
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, T = d.T;
+  const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu, T = d.T;
+  const int nl = (T + 1) * nx, nz = nl + T * nu, sz = nx + nu;
   const Family fam = Family::from(v.prob);
   const double s2 = 2.0 * fam.scale;
-  const long total = static_cast<long>(*n_work) * d.nth;
-  for (long g = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; g < total;
-       g += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int p = work[g / d.nth];
-    const int k = static_cast<int>(g % d.nth);
-    if (v.status[p].code != DOCP_OK) continue;
-    const double* z = v.z + static_cast<long>(p) * d.nz;
-    const double* zt = v.zqp + static_cast<long>(p) * d.nz;
-    const double* lam = v.lam + static_cast<long>(p) * d.nl;
-    const double* lt = v.lt + static_cast<long>(p) * d.nl;
-    double acc = 0.0;
-    if (k < nx) {  // state-cost weights
-      for (int t = 0; t <= T; ++t) acc = acc - s2 * (z[xoff(d, t) + k] * zt[xoff(d, t) + k]);
-    } else if (k < nx + nu) {
-      const int i = k - nx;
-      for (int t = 0; t < T; ++t) acc = acc - s2 * (z[uoff(d, t) + i] * zt[uoff(d, t) + i]);
-    } else if (fam.kind != DOCP_AFFINE_QUADRATIC) {  // initial state (quadratic_cost.hpp:24-45)
-      if (k < 2 * nx + nu) acc = acc + lt[k - nx - nu];  // attitude's inertia tail: 0
-    } else {
-      const int e = k - nx - nu;
-      if (e < nx * nx) {  // dA(i,j) += lam_{t+1,i} z~x_{t,j} + lam~_{t+1,i} x_{t,j}
-        const int i = e % nx, j = e / nx;
-        for (int t = 0; t < T; ++t) {
-          acc = acc + lam[(t + 1) * nx + i] * zt[xoff(d, t) + j];
-          acc = acc + lt[(t + 1) * nx + i] * z[xoff(d, t) + j];
-        }
-      } else if (e < nx * nx + nx * nu) {
-        const int f = e - nx * nx;
-        const int i = f % nx, j = f / nx;
-        for (int t = 0; t < T; ++t) {
-          acc = acc + lam[(t + 1) * nx + i] * zt[uoff(d, t) + j];
-          acc = acc + lt[(t + 1) * nx + i] * z[uoff(d, t) + j];
-        }
-      } else if (e < nx * nx + nx * nu + nx) {
-        const int i = e - nx * nx - nx * nu;
-        for (int t = 0; t < T; ++t) acc = acc + lt[(t + 1) * nx + i];
-      } else {
-        acc = acc + lt[e - nx * nx - nx * nu - nx];
-      }
+  for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
+    const int p = work[w];
+    if (v.status[p].code != DOCP_OK) continue;  // block-uniform
+    const double* z = v.z + static_cast<long>(p) * nz;
+    const double* zt = v.zqp + static_cast<long>(p) * nz;
+    const double* lam = v.lam + static_cast<long>(p) * nl;
+    const double* lt = v.lt + static_cast<long>(p) * nl;
+    if (staged) {
+      double* sz_ = sm_vjp;
+      double* szt = sz_ + nz;
+      double* sl = szt + nz;
+      double* slt = sl + nl;
+      for (int e = threadIdx.x; e < nz; e += blockDim.x) sz_[e] = z[e], szt[e] = zt[e];
+      for (int e = threadIdx.x; e < nl; e += blockDim.x) sl[e] = lam[e], slt[e] = lt[e];
+      z = sz_, zt = szt, lam = sl, lt = slt;
     }
-    v.grad[static_cast<long>(p) * d.nth + k] = acc;
+    __syncthreads();
+    for (int k = threadIdx.x; k < d.nth; k += blockDim.x) {
+      double acc = 0.0;
+      if (k < nx) {  // state-cost weights
+        for (int t = 0; t <= T; ++t) acc = acc - s2 * (z[t * sz + k] * zt[t * sz + k]);
+      } else if (k < nx + nu) {
+        const int i = k - nx;
+        for (int t = 0; t < T; ++t) acc = acc - s2 * (z[t * sz + nx + i] * zt[t * sz + nx + i]);
+      } else if (fam.kind != DOCP_AFFINE_QUADRATIC) {  // initial state (quadratic_cost.hpp:24-45)
+        if (k < 2 * nx + nu) acc = acc + lt[k - nx - nu];  // attitude's inertia tail: 0
+      } else {
+        const int e = k - nx - nu;
+        if (e < nx * nx) {  // dA(i,j) += lam_{t+1,i} z~x_{t,j} + lam~_{t+1,i} x_{t,j}
+          const int j = e / nx, i = e - j * nx;
+          for (int t = 0; t < T; ++t) {
+            acc = acc + lam[(t + 1) * nx + i] * zt[t * sz + j];
+            acc = acc + lt[(t + 1) * nx + i] * z[t * sz + j];
+          }
+        } else if (e < nx * nx + nx * nu) {
+          const int f = e - nx * nx;
+          const int j = f / nx, i = f - j * nx;
+          for (int t = 0; t < T; ++t) {
+            acc = acc + lam[(t + 1) * nx + i] * zt[t * sz + nx + j];
+            acc = acc + lt[(t + 1) * nx + i] * z[t * sz + nx + j];
+          }
+        } else if (e < nx * nx + nx * nu + nx) {
+          const int i = e - nx * nx - nx * nu;
+          for (int t = 0; t < T; ++t) acc = acc + lt[(t + 1) * nx + i];
+        } else {
+          acc = acc + lt[e - nx * nx - nx * nu - nx];
+        }
+      }
+      v.grad[static_cast<long>(p) * d.nth + k] = acc;
+    }
+    __syncthreads();
   }
 }
 
