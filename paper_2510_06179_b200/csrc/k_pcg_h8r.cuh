@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8r(View v, const int* __r
       get(xbuf, pv0, pv1, low);
       finish(own, low, up, out);
     };
-    // out = Phi^-1 x from shared memory (the super block is re-read after the barrier)
+    // out = Phi^-1 x from shared memory. Two exchanges (x_{i+1}, then the
+    // U_i' x_i hand-over) so that each thread reads its half of U_i once for
+    // both U_i' x_i and U_i x_{i+1}: shared-memory traffic is what bounds this
+    // phase, one barrier is cheaper than a second pass over U_i.
     auto matvec_p = [&](const double* xr, double* out) {
       double xf[8], own[4], hand[4], low[4], up[4], xn[8];
       gather(xr, xf);
@@ -238,20 +241,17 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8r(View v, const int* __r
         h8f::load_rows(PdI, bs, dd);
         rows_times(dd, xf, own);
       }
-      {
-        double2 oo[8][2];
-        h8f::load_rows(PuI, bs, oo);
-        trans_times(oo, xr, hand);  // U_i' x_i
-      }
-      put(xbuf, my0, my1, hand);
       __syncthreads();
       get(vbuf, nf0, nf1, xn);
       get(vbuf, nf2, nf3, xn + 4);
       {
         double2 oo[8][2];
         h8f::load_rows(PuI, bs, oo);
+        trans_times(oo, xr, hand);  // U_i' x_i
         rows_times(oo, xn, up);     // U_i x_{i+1}
       }
+      put(xbuf, my0, my1, hand);
+      __syncthreads();
       get(xbuf, pv0, pv1, low);
       finish(own, low, up, out);
     };
