@@ -50,6 +50,9 @@ struct docp_batch {
   std::vector<void*> allocs;
   int max_hist = 0;
   double last_eps_pd = 1e-6;
+  // the stored diagonal blocks are exactly symmetric (assembled on the device,
+  // schur.hpp:145-164); uploaded systems may not be (pcg_kernel_h8s needs it)
+  bool sym_blocks = false;
   // rollout record (docp_rollout / docp_rollout_backward), grown on demand
   docp_dev::RolloutRec roll{};
   int roll_cap = -1;  // episode steps the record holds

@@ -141,6 +141,7 @@ int launch_assemble_th(docp_batch* b, const int* list, const int* count, int n_h
   // NG group buffers + the two-block P_t hand-off between rounds
   const size_t smem = (static_cast<size_t>(NG) * AsmLayout<NX, NU>::GBUF + 2 * AsmLayout<NX, NU>::P2) * sizeof(double);
   auto kern = fast ? assemble_kernel_t<NX, NU, TH, true> : assemble_kernel_t<NX, NU, TH, false>;
+  if (do_schur) b->sym_blocks = true;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TH, smem));
@@ -172,6 +173,7 @@ int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint
   if (nx == 16 && nu == 8) return launch_assemble_t<16, 8>(b, list, count, n_hint, eps_pd, do_schur, fast);
   const int sp = std::max(b->d.bsz, b->d.nx * b->d.nu);
   const size_t smem = static_cast<size_t>(kAsmWarps) * 6 * sp * sizeof(double);
+  if (do_schur) b->sym_blocks = true;
   CUDA_TRY(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   const int grid = std::max(1, std::min(n_hint, b->num_sms * 8));
   ProfScope ps(b, DOCP_PROF_ASSEMBLE);
@@ -549,6 +551,7 @@ int docp_batch_download(docp_batch* b, int32_t field, void* dst, int32_t on_devi
 
 int docp_batch_upload_schur(docp_batch* b, const double* s_diag, const double* s_sub, const double* p_diag,
                             const double* p_super) {
+  if (b) b->sym_blocks = false;
   if (!b) return fail(DOCP_INVALID, "null batch");
   const Dims& d = b->d;
   const int nx = d.nx;

@@ -1,0 +1,381 @@
+// k_pcg_h8s.cuh — K2 FAST mode for n_x = 8, single CTA: pcg_kernel_h8r with
+// BOTH symmetric diagonal blocks (-S_ii and Phi^-1_ii) held in registers in
+// packed form, so the preconditioner product reads only the super-diagonal
+// blocks from shared memory.
+//
+// -S diag and Phi^-1 diag are symmetric by construction (schur.hpp:145-164:
+// sym(Q_0^-1), sym(chi_t), sym(chi_t^-1), and Q_0), so the two threads of a
+// block row split the 36 distinct entries: thread h keeps the upper triangle
+// of its own 4 x 4 diagonal sub-block (10 values) and columns 4+2h, 5+2h of
+// the upper-right 4 x 4 sub-block (8 values). Its product
+//   y_{R_h} = D_hh x_h                       (own sub-block, symmetric)
+//   y_top  += D01[:, c_h] x[c_h]             (h = 0 keeps it, h = 1 sends it)
+//   y[c_h] += D01[:, c_h]' x_top             (h = 1 keeps it, h = 0 sends it)
+// is 32 fmas per thread, as for the full block, plus one 4-value partner
+// exchange. 18 doubles per block instead of 32 leave room for Phi^-1_ii next
+// to -S_ii and L_i; the Phi^-1 half read from shared memory per iteration
+// drops from (2T+1) to T blocks. FAST arithmetic (a different fold order
+// from h8r / h8f; same iteration counts, <= 1e-9 relative).
+//
+// Requires exactly symmetric diagonal blocks: used for systems assembled on
+// the device (docp_batch::sym_blocks); uploaded systems use pcg_kernel_h8r.
+#pragma once
+
+#include "k_pcg_h8r.cuh"
+
+namespace docp_dev {
+
+namespace h8s {
+
+/// Packed upper triangle of a 4 x 4 symmetric block: (a, b), a <= b.
+__host__ __device__ constexpr int tri(int a, int b) { return a * 4 - a * (a - 1) / 2 + (b - a); }
+
+/// Thread h's share of a symmetric 8 x 8 block (see the header comment).
+struct Sym {
+  double o[10];  // D_hh upper triangle
+  double s[4][2];  // D01 rows 0..3, columns 4+2h, 5+2h
+};
+
+/// Loads thread h's share of symmetric block b (block index b for the swizzle) at blk.
+__device__ __forceinline__ void load_sym(const double* blk, int b, int h, Sym& m) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = a; c < 4; ++c) m.o[tri(a, c)] = blk[blk_off(8, b, 4 * h + a, 4 * h + c)];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) m.s[a][k] = blk[blk_off(8, b, a, 4 + 2 * h + k)];
+}
+
+/// My 4 rows of D x (xf: x in logical order, xr: my half).
+__device__ __forceinline__ void sym_times(const Sym& m, const double* xf, const double* xr, int h, double* out) {
+  auto O = [&](int a, int b) { return a <= b ? m.o[tri(a, b)] : m.o[tri(b, a)]; };
+  double own[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double a = fma(O(q, 1), xr[1], O(q, 0) * xr[0]);
+    const double b = fma(O(q, 3), xr[3], O(q, 2) * xr[2]);
+    own[q] = a + b;
+  }
+  const double xc0 = h ? xf[6] : xf[4], xc1 = h ? xf[7] : xf[5];
+  double A[4], Bt[2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) A[q] = fma(m.s[q][1], xc1, m.s[q][0] * xc0);
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    Bt[k] = fma(m.s[3][k], xf[3], fma(m.s[2][k], xf[2], fma(m.s[1][k], xf[1], m.s[0][k] * xf[0])));
+  double recv[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double send = h ? A[q] : (q < 2 ? Bt[q] : 0.0);
+    recv[q] = __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double mine = q < 2 ? recv[q] : Bt[q - 2];  // h = 1: rows 4,5 from the partner, 6,7 own
+    out[q] = h ? own[q] + mine : (own[q] + A[q]) + recv[q];
+  }
+}
+
+}  // namespace h8s
+
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __restrict__ work,
+                                                        const int* __restrict__ n_work, int* __restrict__ counter,
+                                                        double* __restrict__ sol_all, double epsilon,
+                                                        int max_iters_cfg) {
+  extern __shared__ __align__(128) double sm_pcg[];
+  __shared__ __align__(8) uint64_t s_bar[2];  // [0]: staged -S blocks, [1]: Phi^-1 blocks
+  __shared__ int s_next;
+  const Dims d = v.d;
+  const int nl = d.nl, nb = d.nb;
+  const int tid = threadIdx.x;
+  const int R = nb;
+  const int il = tid >> 1, h = tid & 1;
+  const int i = il;
+  const bool act = i < nb;
+  const bool has_next = act && i + 1 < nb;
+  const bool has_prev = i > 0;
+  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int nwk = *n_work;
+
+  double* sPd = sm_pcg;            // [R] Phi^-1 diagonal blocks (current problem)
+  double* sPu = sPd + R * 64;      // [R] Phi^-1 super blocks
+  double* sNd = sPu + R * 64;      // [R] -S diagonal blocks (next problem, staging)
+  double* sNs = sNd + R * 64;      // [R] -S sub blocks
+  double* vbuf = sNs + R * 64;     // [R + 2] x_i halves (slot = row + 1)
+  double* xbuf = vbuf + (R + 2) * 8;
+  double* red = xbuf + (R + 2) * 8;  // [3][8] dot partials
+
+  const int p = i & 1, m = (i >> 1) & 1;
+  h8f::Bases bs;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      bs.o[k][j] = ((k & 1) ? -8 * p : 8 * p) + 4 * ((k >> 1) ? 1 - h : h) + 2 * (j ^ m);
+
+  const int ib = act ? il : nb - 1;
+  const int io = has_next ? il : 0;
+  const double* PdI = sPd + ib * 64;
+  const double* PuI = sPu + io * 64;
+  const double* NdI = sNd + ib * 64;
+  const double* NsI = sNs + io * 64;
+  auto voff = [](int j, int k) { return j * 8 + 2 * (k ^ ((j >> 1) & 3)); };
+  const int sv = ib + 1;
+  const int my0 = voff(sv, 2 * h), my1 = voff(sv, 2 * h + 1);
+  const int nx0 = voff(sv + 1, 2 * h), nx1 = voff(sv + 1, 2 * h + 1);
+  const int pv0 = voff(sv - 1, 2 * h), pv1 = voff(sv - 1, 2 * h + 1);
+  const int nf0 = voff(sv + 1, 0), nf1 = voff(sv + 1, 1), nf2 = voff(sv + 1, 2), nf3 = voff(sv + 1, 3);
+  const uint32_t bd = static_cast<uint32_t>(nb) * 512u, bo = static_cast<uint32_t>(nb - 1) * 512u;
+
+  // next runnable work item (problems that failed earlier are skipped), tid 0 only
+  auto grab = [&]() -> int {
+    int w = atomicAdd(counter, 1);
+    while (w < nwk && v.status[work[w]].code != DOCP_OK) w = atomicAdd(counter, 1);
+    return w;
+  };
+  auto stage_s = [&](int w) {  // -S blocks of work item w -> staging area
+    const double* rec = v.blocks + static_cast<long>(work[w]) * d.blk_stride;
+    mbar_arrive_expect_tx(&s_bar[0], bd + bo);
+    tma_bulk_g2s(sNd, rec + d.s_diag, bd, &s_bar[0]);
+    if (bo) tma_bulk_g2s(sNs, rec + d.s_sub, bo, &s_bar[0]);
+  };
+
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    const int w = grab();
+    s_next = w;
+    if (w < nwk) stage_s(w);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  const int max_iters = max_iters_cfg > 0 ? max_iters_cfg : 2 * nl;
+  const double threshold = epsilon * epsilon;
+
+  auto partial = [&](const double* a, const double* b, int slot) {
+    double s = fma(a[3], b[3], fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0])));
+    s = act ? s : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) red[slot * 8 + warp] = s;
+  };
+  auto total = [&](int slot) -> double {
+    double t = red[slot * 8];
+    for (int k = 1; k < 8; ++k)
+      if (k < nw) t = t + red[slot * 8 + k];
+    return t;
+  };
+  auto dot = [&](const double* a, const double* b) -> double {
+    partial(a, b, 0);
+    __syncthreads();
+    return total(0);
+  };
+  auto norm = [&](const double* a) -> double {
+    __syncthreads();
+    partial(a, a, 2);
+    __syncthreads();
+    return sqrt(total(2));
+  };
+  auto gather = [&](const double* xr, double* xf) {  // x_i in logical order
+    double other[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) other[q] = __shfl_xor_sync(0xffffffffu, xr[q], 1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      xf[q] = h8f::sel(h, other[q], xr[q]);
+      xf[4 + q] = h8f::sel(h, xr[q], other[q]);
+    }
+  };
+  auto rows_times = [&](const double2 (&mm)[8][2], const double* xf, double* out) {  // my rows of M x
+    double a[4], b[4];
+    a[0] = mm[0][0].x * xf[0], a[1] = mm[0][0].y * xf[0], a[2] = mm[0][1].x * xf[0], a[3] = mm[0][1].y * xf[0];
+    b[0] = mm[4][0].x * xf[4], b[1] = mm[4][0].y * xf[4], b[2] = mm[4][1].x * xf[4], b[3] = mm[4][1].y * xf[4];
+#pragma unroll
+    for (int c = 1; c < 4; ++c) {
+      a[0] = fma(mm[c][0].x, xf[c], a[0]);
+      a[1] = fma(mm[c][0].y, xf[c], a[1]);
+      a[2] = fma(mm[c][1].x, xf[c], a[2]);
+      a[3] = fma(mm[c][1].y, xf[c], a[3]);
+      b[0] = fma(mm[4 + c][0].x, xf[4 + c], b[0]);
+      b[1] = fma(mm[4 + c][0].y, xf[4 + c], b[1]);
+      b[2] = fma(mm[4 + c][1].x, xf[4 + c], b[2]);
+      b[3] = fma(mm[4 + c][1].y, xf[4 + c], b[3]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = a[q] + b[q];
+  };
+  auto trans_times = [&](const double2 (&mm)[8][2], const double* xm, double* out) {  // my 4 entries of M' x
+    double part[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      part[c] = fma(mm[c][1].y, xm[3], fma(mm[c][1].x, xm[2], fma(mm[c][0].y, xm[1], mm[c][0].x * xm[0])));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double send = h8f::sel(h, part[q], part[4 + q]);
+      const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+      out[q] = h8f::sel(h, part[4 + q], part[q]) + recv;
+    }
+  };
+  auto put = [&](double* buf, int o0, int o1, const double* x) {
+    if (act) {
+      *reinterpret_cast<double2*>(buf + o0) = make_double2(x[0], x[1]);
+      *reinterpret_cast<double2*>(buf + o1) = make_double2(x[2], x[3]);
+    }
+  };
+  auto get = [&](const double* buf, int o0, int o1, double* x) {
+    const double2 a = *reinterpret_cast<const double2*>(buf + o0);
+    const double2 b = *reinterpret_cast<const double2*>(buf + o1);
+    x[0] = a.x, x[1] = a.y, x[2] = b.x, x[3] = b.y;
+  };
+  auto finish = [&](const double* own, const double* low, const double* up, double* out) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // diag, then sub (i > 0), then super (i < nb - 1)
+      double acc = own[q];
+      acc = has_prev ? acc + low[q] : acc;
+      acc = has_next ? acc + up[q] : acc;
+      out[q] = acc;
+    }
+  };
+
+  h8s::Sym sd, pd;  // my shares of -S_ii and Phi^-1_ii, resident for the whole solve
+  double2 so[8][2];  // my rows of L_i
+
+  for (;;) {
+    const int w = s_next;
+    if (w >= nwk) break;
+    const int pidx = work[w];
+    mbar_wait(&s_bar[0], phase);
+    h8s::load_sym(NdI, ib, h, sd);
+    h8f::load_rows(NsI, bs, so);
+    __syncthreads();  // staging area consumed; the previous problem's Phi^-1 reads are long done
+    if (tid == 0) {
+      fence_proxy_async();
+      const double* rec = v.blocks + static_cast<long>(pidx) * d.blk_stride;
+      mbar_arrive_expect_tx(&s_bar[1], bd + bo);
+      tma_bulk_g2s(sPd, rec + d.p_diag, bd, &s_bar[1]);
+      if (bo) tma_bulk_g2s(sPu, rec + d.p_sup, bo, &s_bar[1]);
+      const int wn = grab();
+      s_next = wn;  // read after the end-of-problem barrier
+      if (wn < nwk) stage_s(wn);
+    }
+    const double* gam = v.gamma + static_cast<long>(pidx) * nl;
+    double* sol = sol_all + static_cast<long>(pidx) * nl;
+
+    double lam[4] = {0, 0, 0, 0}, r[4], pv[4], y[4];
+    if (act) {
+      const double2 a = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h);
+      const double2 b = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h + 2);
+      lam[0] = a.x, lam[1] = a.y, lam[2] = b.x, lam[3] = b.y;
+    }
+
+    // out = (-S) x from the register-resident blocks
+    auto matvec_s = [&](const double* xr, double* out) {
+      double xf[8], own[4], hand[4], low[4], up[4], xn[4];
+      gather(xr, xf);
+      put(vbuf, my0, my1, xr);
+      h8s::sym_times(sd, xf, xr, h, own);
+      rows_times(so, xf, hand);  // L_i x_i
+      put(xbuf, my0, my1, hand);
+      __syncthreads();
+      get(vbuf, nx0, nx1, xn);
+      trans_times(so, xn, up);   // L_i' x_{i+1}
+      get(xbuf, pv0, pv1, low);
+      finish(own, low, up, out);
+    };
+    // out = Phi^-1 x from shared memory. Two exchanges (x_{i+1}, then the
+    // U_i' x_i hand-over) so that each thread reads its half of U_i once for
+    // both U_i' x_i and U_i x_{i+1}: shared-memory traffic is what bounds this
+    // phase, one barrier is cheaper than a second pass over U_i.
+    auto matvec_p = [&](const double* xr, double* out) {
+      double xf[8], own[4], hand[4], low[4], up[4], xn[8];
+      gather(xr, xf);
+      put(vbuf, my0, my1, xr);
+      h8s::sym_times(pd, xf, xr, h, own);
+      __syncthreads();
+      get(vbuf, nf0, nf1, xn);
+      get(vbuf, nf2, nf3, xn + 4);
+      {
+        double2 oo[8][2];
+        h8f::load_rows(PuI, bs, oo);
+        trans_times(oo, xr, hand);  // U_i' x_i
+        rows_times(oo, xn, up);     // U_i x_{i+1}
+      }
+      put(xbuf, my0, my1, hand);
+      __syncthreads();
+      get(xbuf, pv0, pv1, low);
+      finish(own, low, up, out);
+    };
+
+    matvec_s(lam, y);  // y = (-S) lambda0
+    if (act) {
+      const double2 a = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h);
+      const double2 b = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h + 2);
+      r[0] = a.x - y[0], r[1] = a.y - y[1], r[2] = b.x - y[2], r[3] = b.y - y[3];
+    } else {
+      r[0] = r[1] = r[2] = r[3] = 0.0;
+    }
+    __syncthreads();  // every phase-2 read of lambda / its hand-over is done
+    mbar_wait(&s_bar[1], phase);
+    phase ^= 1;
+    h8s::load_sym(PdI, ib, h, pd);
+    matvec_p(r, pv);  // r~
+    double eta = dot(r, pv);
+    int status = DOCP_OK, iters = 0;
+    if (eta < 0.0) {
+      const double scale = norm(r) * norm(pv);
+      if (-eta <= 1e-10 * scale + 1e-300) eta = 0.0;
+      else status = DOCP_AT_PCG_PRECOND;
+    }
+
+    while (status == DOCP_OK && eta > threshold && iters < max_iters) {
+      matvec_s(pv, y);
+      const double vv = dot(pv, y);
+      if (vv <= 0.0) {
+        status = DOCP_AT_PCG_CURVATURE;
+        break;
+      }
+      const double alpha = eta / vv;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        lam[q] = fma(alpha, pv[q], lam[q]);
+        r[q] = fma(-alpha, y[q], r[q]);
+      }
+      matvec_p(r, y);  // r~ (y reused)
+      double eta_next = dot(r, y);
+      if (eta_next < 0.0) {
+        const double scale = norm(r) * norm(y);
+        if (-eta_next <= 1e-10 * scale + 1e-300) {
+          eta_next = 0.0;
+        } else {
+          status = DOCP_AT_PCG_PRECOND;
+          break;
+        }
+      }
+      const double beta = eta_next / eta;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pv[q] = fma(beta, pv[q], y[q]);
+      eta = eta_next;
+      ++iters;
+    }
+
+    if (act) {
+      *reinterpret_cast<double2*>(sol + i * 8 + 4 * h) = make_double2(lam[0], lam[1]);
+      *reinterpret_cast<double2*>(sol + i * 8 + 4 * h + 2) = make_double2(lam[2], lam[3]);
+    }
+    if (tid == 0) {
+      v.pcg_iters[pidx] = iters;
+      v.final_eta[pidx] = eta;
+      v.pcg_conv[pidx] = status == DOCP_OK && eta <= threshold;
+      if (status == DOCP_OK) set_status(v.status + pidx, DOCP_OK, DOCP_AT_NONE, 0);
+      else set_status(v.status + pidx, DOCP_BREAKDOWN, status, iters);
+      atomicAdd(v.pcg_acc, static_cast<unsigned long long>(iters));
+      atomicAdd(v.pcg_acc + 1, 1ull);
+      atomicAdd(v.pcg_acc + 2, 1ull);  // lifetime solves (docp_pcg_invocations)
+    }
+    __syncthreads();  // s_next is published; Phi^-1 / vectors free for the next problem
+  }
+}
+
+}  // namespace docp_dev

@@ -5,6 +5,7 @@
 #include "k_pcg_h8.cuh"
 #include "k_pcg_h8f.cuh"
 #include "k_pcg_h8r.cuh"
+#include "k_pcg_h8s.cuh"
 #include "pcg_launch.cuh"
 
 namespace docp_host {
@@ -85,6 +86,25 @@ static int launch_h8r(docp_batch* b, const int* list, const int* count, int n_hi
   return DOCP_OK;
 }
 
+/// FAST, one CTA per problem, device-assembled (symmetric) diagonal blocks:
+/// pcg_kernel_h8s (both diagonal blocks in registers).
+static int launch_h8s(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
+                      int max_iters) {
+  auto kern = pcg_kernel_h8s<256>;
+  const size_t smem = h8r_smem_doubles(b->d) * sizeof(double);
+  const int threads = (2 * b->d.nb + 31) / 32 * 32;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit on an SM (smem %zu)", smem);
+  const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
+  CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
+  ProfScope ps(b, DOCP_PROF_PCG);
+  kern<<<grid, threads, smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
 /// Smallest cluster (1, 2, 4, 8) whose per-CTA share of the blocks fits in
 /// shared memory with at most 128 block rows per CTA; 0 if none.
 int h8f_cluster_for(const Dims& d, int device) {
@@ -117,8 +137,9 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
   if (!par && !force_h8()) {
     switch (h8f_cluster(b)) {
       case 1:
-        if (!force_variant("h8f")) return launch_h8r(b, list, count, n_hint, sol, eps, max_iters);
-        return launch_h8f_cl<1>(b, list, count, n_hint, sol, eps, max_iters);
+        if (force_variant("h8f")) return launch_h8f_cl<1>(b, list, count, n_hint, sol, eps, max_iters);
+        if (b->sym_blocks && !force_variant("h8r")) return launch_h8s(b, list, count, n_hint, sol, eps, max_iters);
+        return launch_h8r(b, list, count, n_hint, sol, eps, max_iters);
       case 2: return launch_h8f_cl<2>(b, list, count, n_hint, sol, eps, max_iters);
       case 4: return launch_h8f_cl<4>(b, list, count, n_hint, sol, eps, max_iters);
       case 8: return launch_h8f_cl<8>(b, list, count, n_hint, sol, eps, max_iters);

@@ -515,10 +515,12 @@ def test_pcg_breakdown_all_kernels(D, nx, nu, T):
 
 
 @pytest.mark.parametrize("nx,nu,T", [(8, 4, 1), (8, 4, 2), (8, 4, 30), (8, 4, 100), (8, 4, 113)])
-def test_fast_nx8_kernels_agree_bitwise(D, nx, nu, T, monkeypatch):
-    """The n_x = 8 single-CTA FAST kernels fold every sum in the same order:
-    pcg_kernel_h8r (-S in registers, the default) and pcg_kernel_h8f return
-    bit-identical iterates and counts."""
+def test_fast_nx8_kernels_agree(D, nx, nu, T, monkeypatch):
+    """The n_x = 8 single-CTA FAST kernels: pcg_kernel_h8r (-S in registers)
+    and pcg_kernel_h8f fold every sum in the same order and agree bit for bit;
+    pcg_kernel_h8s (the default for device-assembled systems: both symmetric
+    diagonal blocks packed in registers) folds the diagonal products in
+    another order: same iteration counts, iterates within 1e-12."""
     th = aq_thetas(nx, nu, T, 77, 5)
     b = D.Batch(D.affine_quadratic(nx, nu, T), 5)
     b.upload(D._lib.F_THETA, th)
@@ -527,11 +529,12 @@ def test_fast_nx8_kernels_agree_bitwise(D, nx, nu, T, monkeypatch):
     b.assemble_schur()
     b.assemble_gamma()
     got = {}
-    for variant in ("", "h8f"):
+    for variant in ("", "h8r", "h8f"):
         monkeypatch.setenv("DOCP_PCG_VARIANT", variant)
         b.upload(D._lib.F_LAMBDA, np.zeros((5, b.nl)))
         b.pcg_solve(D.PcgConfig(mode="fast"))
         got[variant] = (b.download(D._lib.F_LAMBDA), b.download(D._lib.F_PCG_ITERS)[:, 0])
-    for variant in ("h8f",):
-        assert np.array_equal(got[variant][1], got[""][1]), variant
-        assert np.array_equal(got[variant][0], got[""][0]), variant
+    assert np.array_equal(got["h8f"][1], got["h8r"][1]) and np.array_equal(got["h8f"][0], got["h8r"][0])
+    assert np.array_equal(got[""][1], got["h8r"][1])
+    for j in range(5):
+        assert rel(got[""][0][j], got["h8r"][0][j]) <= 1e-12
