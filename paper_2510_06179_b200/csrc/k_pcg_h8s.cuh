@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
     if (bo) tma_bulk_g2s(sNs, rec + d.s_sub, bo, &s_bar[0]);
   };
 
+  if (tid < 24) red[tid] = 0.0;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -161,11 +162,11 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
     s = warp_sum(s);
     if (lane == 0) red[slot * 8 + warp] = s;
   };
+  // pairwise over the 8 warp slots (slots of absent warps hold 0): depth 3
   auto total = [&](int slot) -> double {
-    double t = red[slot * 8];
-    for (int k = 1; k < 8; ++k)
-      if (k < nw) t = t + red[slot * 8 + k];
-    return t;
+    const double2* q = reinterpret_cast<const double2*>(red + slot * 8);
+    const double2 a = q[0], b = q[1], c = q[2], e = q[3];
+    return ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (e.x + e.y));
   };
   auto dot = [&](const double* a, const double* b) -> double {
     partial(a, b, 0);
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
     h8s::load_sym(PdI, ib, h, pd);
     matvec_p(r, pv);  // r~
     double eta = dot(r, pv);
+    double inv_eta = 1.0 / eta;  // beta = eta' / eta as eta' * (1 / eta), the division off the critical path
     int status = DOCP_OK, iters = 0;
     if (eta < 0.0) {
       const double scale = norm(r) * norm(pv);
@@ -353,10 +355,11 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
           break;
         }
       }
-      const double beta = eta_next / eta;
+      const double beta = eta_next * inv_eta;
 #pragma unroll
       for (int q = 0; q < 4; ++q) pv[q] = fma(beta, pv[q], y[q]);
       eta = eta_next;
+      inv_eta = 1.0 / eta;
       ++iters;
     }
 
