@@ -39,6 +39,145 @@ struct AsmShared {
   int rank_lin, rank_qr, rank_chi, proj;
 };
 
+/// Phase A for the affine-quadratic family with compile-time block sizes:
+/// one thread per ENTRY instead of one per stage task, so the CTA's threads
+/// share the work evenly and every store is coalesced. A stage's entries are
+/// NX (NU) consecutive lanes of one warp; the per-stage decisions of the
+/// reference (project_pd's LLT test, the finiteness checks, problem.hpp:157-
+/// 257) are warp-ballots over the stage's lanes, and the first failure is
+/// ranked exactly as the per-stage path ranks it. Values and expression
+/// order per entry are those of the per-stage path.
+template <int NX, int NU>
+__device__ void linearize_aq_rows(const View& v, int p, double eps_pd, const Family& fam, const double* z,
+                                  const double* th, AsmShared& sh) {
+  const Dims d = v.d;
+  const int T = d.T, sz = NX + NU;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const double* wx = th;
+  const double* wu = th + NX;
+  const double* ath = th + NX + NU;          // A, column-major (affine_quadratic.hpp:27-37)
+  const double* bth = ath + NX * NX;         // B
+  const double* off = bth + NX * NU;         // b
+  double* qd = v.qd + static_cast<long>(p) * d.nb * NX;
+  double* lq = v.lq + static_cast<long>(p) * d.nb * NX;
+  double* q = v.q + static_cast<long>(p) * d.nb * NX;
+  double* rd = v.rd + static_cast<long>(p) * T * NU;
+  double* lr = v.lr + static_cast<long>(p) * T * NU;
+  double* r = v.r + static_cast<long>(p) * T * NU;
+  double* Cm = v.C + static_cast<long>(p) * T * NX;
+  double* jx = v.A + a_off(d, p, 0);
+  double* ju = v.Bm + b_off(d, p, 0);
+  // all lanes of a stage group agree (ballot over the group's lanes)
+  auto group_all = [&](bool pred, int n) {
+    const unsigned bal = __ballot_sync(0xffffffffu, pred);
+    const unsigned gm = (n == 32 ? 0xffffffffu : ((1u << n) - 1u)) << (lane & ~(n - 1));
+    return (bal & gm) == gm;
+  };
+  auto group_any = [&](bool pred, int n) {
+    const unsigned bal = __ballot_sync(0xffffffffu, pred);
+    const unsigned gm = (n == 32 ? 0xffffffffu : ((1u << n) - 1u)) << (lane & ~(n - 1));
+    return (bal & gm) != 0u;
+  };
+  const int nstate = (T + 1) * NX, nctrl = T * NU, ndyn = T * NX;
+  // ---- state cost entries (problem.hpp:221-230)
+  for (int base = 0; base < nstate; base += blockDim.x) {
+    const int k = base + tid;
+    const bool valid = k < nstate;
+    const int t = valid ? k / NX : 0, i = k - (k / NX) * NX;
+    const double* x = z + t * sz;
+    const double h = diag_cost_hess(fam.scale, wx[i]);
+    const double g = diag_cost_grad(fam.scale, wx[i], x[i]);
+    bool fin = isfinite(g) && isfinite(h);
+    if (i == 0) fin = fin && isfinite(diag_cost_value<NX>(fam.scale, wx, x, NX));
+    const bool finite = group_all(fin || !valid, NX);
+    const bool pass = group_all(h - eps_pd * 1.0 > 0.0, NX);
+    const bool below = group_any(h < eps_pd, NX);
+    const bool modified = NX == 1 ? below : !pass;
+    if (valid) {
+      if (!finite && i == 0) atomicMin(&sh.rank_lin, t);
+      if (modified) sh.proj = 1;
+      const double hq = modified ? (h < eps_pd ? eps_pd : h) : h;
+      qd[k] = hq;
+      q[k] = g - hq * x[i];
+      if (!(hq > 0.0) && !isnan(hq)) atomicMin(&sh.rank_qr, t);  // chol_Q (schur.hpp:131-133)
+      lq[k] = sqrt(hq);
+    }
+  }
+  // ---- control cost entries (problem.hpp:231-240)
+  for (int base = 0; base < nctrl; base += blockDim.x) {
+    const int k = base + tid;
+    const bool valid = k < nctrl;
+    const int t = valid ? k / NU : 0, i = k - (k / NU) * NU;
+    const double* u = z + t * sz + NX;
+    const double h = diag_cost_hess(fam.scale, wu[i]);
+    const double g = diag_cost_grad(fam.scale, wu[i], u[i]);
+    bool fin = isfinite(g) && isfinite(h);
+    if (i == 0) fin = fin && isfinite(diag_cost_value<NU>(fam.scale, wu, u, NU));
+    const bool finite = group_all(fin || !valid, NU);
+    const bool pass = group_all(h - eps_pd * 1.0 > 0.0, NU);
+    const bool below = group_any(h < eps_pd, NU);
+    const bool modified = NU == 1 ? below : !pass;
+    if (valid) {
+      if (!finite && i == 0) atomicMin(&sh.rank_lin, T + 1 + 2 * t);
+      if (modified) sh.proj = 1;
+      const double hr = modified ? (h < eps_pd ? eps_pd : h) : h;
+      rd[k] = hr;
+      r[k] = g - hr * u[i];
+      if (!(hr > 0.0) && !isnan(hr)) atomicMin(&sh.rank_qr, T + 1 + t);
+      lr[k] = sqrt(hr);
+    }
+  }
+  // ---- dynamics rows (affine_quadratic.hpp:65-75, problem.hpp:241-252)
+  for (int base = 0; base < ndyn; base += blockDim.x) {
+    const int k = base + tid;
+    const bool valid = k < ndyn;
+    const int t = valid ? k / NX : 0, i = k - (k / NX) * NX;
+    const double* x = z + t * sz;
+    const double* u = x + NX;
+    const double* xn = z + (t + 1) * sz;
+    double ax = ath[i] * x[0];
+#pragma unroll
+    for (int c = 1; c < NX; ++c) ax = ax + ath[i + c * NX] * x[c];
+    double bu = bth[i] * u[0];
+#pragma unroll
+    for (int c = 1; c < NU; ++c) bu = bu + bth[i + c * NX] * u[c];
+    const double res = ((xn[i] - ax) - bu) - off[i];
+    bool fin = isfinite(res);
+    if (t == 0) {  // the time-invariant Jacobians, written once: jac_x = -A, jac_u = -B
+#pragma unroll
+      for (int c = 0; c < NX; ++c) fin = fin && isfinite(-ath[i + c * NX]);
+#pragma unroll
+      for (int c = 0; c < NU; ++c) fin = fin && isfinite(-bth[i + c * NX]);
+      if (valid) {
+#pragma unroll
+        for (int c = 0; c < NX; ++c) jx[i + c * NX] = -ath[i + c * NX];
+#pragma unroll
+        for (int c = 0; c < NU; ++c) ju[i + c * NX] = -bth[i + c * NX];
+      }
+    }
+    const bool finite = group_all(fin || !valid, NX);
+    if (valid) {
+      if (!finite && i == 0) atomicMin(&sh.rank_lin, T + 2 + 2 * t);
+      // C_t = A+ x+ + A x + B u - f, with the Jacobians at z (problem.hpp:250-251)
+      double cx = (-ath[i]) * x[0];
+#pragma unroll
+      for (int c = 1; c < NX; ++c) cx = cx + (-ath[i + c * NX]) * x[c];
+      double cu = (-bth[i]) * u[0];
+#pragma unroll
+      for (int c = 1; c < NU; ++c) cu = cu + (-bth[i + c * NX]) * u[c];
+      Cm[k] = ((xn[i] + cx) + cu) - res;
+    }
+  }
+  // ---- initial state (problem.hpp:253-254)
+  if (tid < 32) {
+    const double* x_s = fam.x_s(d, th);
+    const bool valid = tid < NX;
+    const double xv = valid ? x_s[tid] : 0.0;
+    if (valid) v.xs[static_cast<long>(p) * NX + tid] = xv;
+    if (!__all_sync(0xffffffffu, !valid || isfinite(xv)) && tid == 0) atomicMin(&sh.rank_lin, 3 * T + 1);
+  }
+}
+
 /// Phase A of K1 (problem.hpp:202-257): one thread per stage task. Writes the
 /// QpData of problem p and the first-error ranks; returns (block-uniform)
 /// whether the Schur phases may run. Ends with a __syncthreads. NX, NU > 0
@@ -79,6 +218,12 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
   __syncthreads();
   const double* wx = fam.w_x(d, th);
   const double* wu = fam.w_u(d, th);
+  if constexpr (NX > 0 && NU > 0 && kWarp % NX == 0 && kWarp % NU == 0) {
+    if (fam.kind == DOCP_AFFINE_QUADRATIC && !tv) {
+      linearize_aq_rows<NX, NU>(v, p, eps_pd, fam, z, th, sh);
+      goto tasks_done;
+    }
+  }
   for (int task = tid; task < 2 * T + 2; task += blockDim.x) {
     if (task <= T) {  // state cost at x_t (problem.hpp:221-230)
       const int t = task;
@@ -163,6 +308,7 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
       if (!fin) atomicMin(&sh.rank_lin, 3 * T + 1);
     }
   }
+tasks_done:
   __syncthreads();
   const int rank_lin = sh.rank_lin, rank_qr = sh.rank_qr;
   if (tid == 0) {

@@ -197,6 +197,44 @@ def test_assembly_bitwise(D, nx, nu, T, seed):
         assert np.array_equal(gam[j], o.gamma(o.flat_b(), o.flat_d()))
 
 
+@pytest.mark.parametrize("nx,nu,T", [(8, 4, 20), (4, 2, 12), (4, 1, 9), (5, 2, 9)])
+def test_linearize_errors_and_projection(D, nx, nu, T):
+    """K1 phase A (per-entry for compile-time affine-quadratic shapes, per-stage
+    otherwise): the first failing stage in the reference's order, the
+    project_pd clamps and the QpData, against the oracle."""
+    B = 8
+    th = aq_thetas(nx, nu, T, 5, B)
+    rng = np.random.default_rng(9)
+    prob = D.affine_quadratic(nx, nu, T)
+    b = D.Batch(prob, B)
+    z = rng.standard_normal((B, b.nz))
+    sz = nx + nu
+    th[1, 2 % nx] = 1e-9                     # Q below eps_pd: projected (problem.hpp:157-181)
+    th[2, nx] = -1.0                         # R indefinite: projected
+    z[3, 7 % T * sz + 1 % nx] = 1e200        # state cost overflows at stage 7 % T
+    z[4, 3 % T * sz + nx] = np.inf           # control (and dynamics) at stage 3 % T
+    th[5, nx + nu + 1] = np.nan              # A: dynamics non-finite from stage 0
+    z[6, T * sz] = np.nan                    # terminal state
+    th[7, -1] = np.nan                       # x_s
+    b.upload(D._lib.F_THETA, th)
+    b.upload(D._lib.F_Z, z)
+    b.linearize()
+    errs = b.errors()
+    qp = b.download_qp()
+    for j in range(B):
+        o = po.Oracle("port", po.aq_problem(nx, nu, T))
+        try:
+            o.linearize(th[j], z[j])
+        except po.OracleError as e:
+            assert errs[j] is not None and str(errs[j]) == e.message, (j, errs[j], e.message)
+            continue
+        assert errs[j] is None, (j, errs[j])
+        oq = o.qp()
+        for k in ("Q", "q", "R", "r", "A", "B", "C", "x_s"):
+            assert np.array_equal(qp[k][j], oq[k]), (j, k)
+    assert [e is None for e in errs] == [True, True, True, False, False, False, False, False]
+
+
 def test_assembly_cartpole(D):
     x0, demos = _cartpole_demos(4)
     prob = D.cartpole(40)
