@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
                                                         int max_iters_cfg) {
   extern __shared__ __align__(128) double sm_pcg[];
   __shared__ __align__(8) uint64_t s_bar[2];  // [0]: staged -S blocks, [1]: Phi^-1 blocks
-  __shared__ int s_next;
+  __shared__ int s_next, s_pidx;
   const Dims d = v.d;
   const int nl = d.nl, nb = d.nb;
   const int tid = threadIdx.x;
@@ -130,14 +130,16 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
   const int nf0 = voff(sv + 1, 0), nf1 = voff(sv + 1, 1), nf2 = voff(sv + 1, 2), nf3 = voff(sv + 1, 3);
   const uint32_t bd = static_cast<uint32_t>(nb) * 512u, bo = static_cast<uint32_t>(nb - 1) * 512u;
 
-  // next runnable work item (problems that failed earlier are skipped), tid 0 only
-  auto grab = [&]() -> int {
-    int w = atomicAdd(counter, 1);
-    while (w < nwk && v.status[work[w]].code != DOCP_OK) w = atomicAdd(counter, 1);
-    return w;
+  // next work item and its problem index (tid 0 only). Problems that failed
+  // earlier are skipped at the start of their turn (all threads read the
+  // status there), which keeps tid 0's chain to one atomic and one load.
+  auto grab = [&]() {
+    const int w = atomicAdd(counter, 1);
+    s_next = w;
+    s_pidx = w < nwk ? work[w] : 0;
   };
-  auto stage_s = [&](int w) {  // -S blocks of work item w -> staging area
-    const double* rec = v.blocks + static_cast<long>(work[w]) * d.blk_stride;
+  auto stage_s = [&](int pi) {  // -S blocks of problem pi -> staging area
+    const double* rec = v.blocks + static_cast<long>(pi) * d.blk_stride;
     mbar_arrive_expect_tx(&s_bar[0], bd + bo);
     tma_bulk_g2s(sNd, rec + d.s_diag, bd, &s_bar[0]);
     if (bo) tma_bulk_g2s(sNs, rec + d.s_sub, bo, &s_bar[0]);
@@ -147,12 +149,11 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
-    const int w = grab();
-    s_next = w;
-    if (w < nwk) stage_s(w);
+    grab();
+    if (s_next < nwk) stage_s(s_pidx);
   }
   __syncthreads();
-  uint32_t phase = 0;
+  uint32_t phase = 0, ph1 = 0;  // parities of s_bar[0] (staging) and s_bar[1] (Phi^-1)
   const int max_iters = max_iters_cfg > 0 ? max_iters_cfg : 2 * nl;
   const double threshold = epsilon * epsilon;
 
@@ -246,30 +247,44 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
   for (;;) {
     const int w = s_next;
     if (w >= nwk) break;
-    const int pidx = work[w];
+    const int pidx = s_pidx;
+    // this problem's warm start and right-hand side, issued before the
+    // staging wait so their latency overlaps it
+    const double* gam = v.gamma + static_cast<long>(pidx) * nl;
+    double* sol = sol_all + static_cast<long>(pidx) * nl;
+    double2 l01 = make_double2(0.0, 0.0), l23 = l01, g01 = l01, g23 = l01;
+    if (act) {
+      l01 = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h);
+      l23 = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h + 2);
+      g01 = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h);
+      g23 = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h + 2);
+    }
+    const bool runnable = v.status[pidx].code == DOCP_OK;  // failed in an earlier stage: skip
     mbar_wait(&s_bar[0], phase);
     h8s::load_sym(NdI, ib, h, sd);
     h8f::load_rows(NsI, bs, so);
-    __syncthreads();  // staging area consumed; the previous problem's Phi^-1 reads are long done
+    __syncthreads();  // staging area consumed; s_next / s_pidx read; Phi^-1 reads of the previous problem done
+    phase ^= 1;
+    if (!runnable) {  // block-uniform; s_bar[1] is not armed for a skipped problem
+      if (tid == 0) {
+        fence_proxy_async();
+        grab();
+        if (s_next < nwk) stage_s(s_pidx);
+      }
+      __syncthreads();
+      continue;
+    }
     if (tid == 0) {
       fence_proxy_async();
       const double* rec = v.blocks + static_cast<long>(pidx) * d.blk_stride;
       mbar_arrive_expect_tx(&s_bar[1], bd + bo);
       tma_bulk_g2s(sPd, rec + d.p_diag, bd, &s_bar[1]);
       if (bo) tma_bulk_g2s(sPu, rec + d.p_sup, bo, &s_bar[1]);
-      const int wn = grab();
-      s_next = wn;  // read after the end-of-problem barrier
-      if (wn < nwk) stage_s(wn);
+      grab();  // s_next / s_pidx: read after the end-of-problem barrier
+      if (s_next < nwk) stage_s(s_pidx);
     }
-    const double* gam = v.gamma + static_cast<long>(pidx) * nl;
-    double* sol = sol_all + static_cast<long>(pidx) * nl;
 
-    double lam[4] = {0, 0, 0, 0}, r[4], pv[4], y[4];
-    if (act) {
-      const double2 a = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h);
-      const double2 b = *reinterpret_cast<const double2*>(sol + i * 8 + 4 * h + 2);
-      lam[0] = a.x, lam[1] = a.y, lam[2] = b.x, lam[3] = b.y;
-    }
+    double lam[4] = {l01.x, l01.y, l23.x, l23.y}, r[4], pv[4], y[4];
 
     // out = (-S) x from the register-resident blocks
     auto matvec_s = [&](const double* xr, double* out) {
@@ -311,15 +326,13 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
 
     matvec_s(lam, y);  // y = (-S) lambda0
     if (act) {
-      const double2 a = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h);
-      const double2 b = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h + 2);
-      r[0] = a.x - y[0], r[1] = a.y - y[1], r[2] = b.x - y[2], r[3] = b.y - y[3];
+      r[0] = g01.x - y[0], r[1] = g01.y - y[1], r[2] = g23.x - y[2], r[3] = g23.y - y[3];
     } else {
       r[0] = r[1] = r[2] = r[3] = 0.0;
     }
     __syncthreads();  // every phase-2 read of lambda / its hand-over is done
-    mbar_wait(&s_bar[1], phase);
-    phase ^= 1;
+    mbar_wait(&s_bar[1], ph1);
+    ph1 ^= 1;
     h8s::load_sym(PdI, ib, h, pd);
     matvec_p(r, pv);  // r~
     double eta = dot(r, pv);

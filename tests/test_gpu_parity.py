@@ -369,17 +369,27 @@ def test_il_epoch_matches_oracle(D):
         wt = torch.tensor(w, device=dev)
 
 
-def test_error_statuses(D):
+@pytest.mark.parametrize("nx,nu,T", [(4, 2, 10), (8, 4, 30)])
+def test_error_statuses(D, nx, nu, T):
     """Per-problem failures become the reference's errors; the rest of the
-    batch is unaffected (batch.hpp:92-101)."""
-    nx, nu, T = 4, 2, 10
-    th = aq_thetas(nx, nu, T, 31, 3)
-    th[1, -nx] = np.nan  # non-finite x_s (test_batch.cpp:88-105)
+    batch is unaffected (batch.hpp:92-101). The PCG kernels skip the failed
+    problems of their work list (n_x = 8: pcg_kernel_h8s's skip path)."""
+    B = 7
+    th = aq_thetas(nx, nu, T, 31, B)
+    for j in (1, 3, 4):
+        th[j, -nx] = np.nan  # non-finite x_s (test_batch.cpp:88-105)
     prob = D.affine_quadratic(nx, nu, T)
     nz, nl = D.sizes(prob)
-    res, errs = D.sqp_solve_batch(prob, th, np.zeros((3, nz)), np.zeros((3, nl)), D.SqpConfig())
-    assert errs[0] is None and errs[2] is None
-    assert isinstance(errs[1], D.EvaluationError) and "initial_state" in str(errs[1])
+    res, errs = D.sqp_solve_batch(prob, th, np.zeros((B, nz)), np.zeros((B, nl)),
+                                  D.SqpConfig(pcg=D.PcgConfig(mode="fast")))
+    for j in range(B):
+        if j in (1, 3, 4):
+            assert isinstance(errs[j], D.EvaluationError) and "initial_state" in str(errs[j])
+            continue
+        assert errs[j] is None
+        o = po.Oracle("port", po.aq_problem(nx, nu, T))
+        s = o.sqp_solve(th[j], np.zeros(nz), np.zeros(nl), po.sqp_config())
+        assert res[j].pcg_iters == s.pcg_iters and rel(res[j].z, s.z) <= RTOL_FAST
     with pytest.raises(D.DimensionError):
         D.sqp_solve(prob, th[0], np.full(nz, np.inf), np.zeros(nl))
     with pytest.raises(D.DimensionError):
