@@ -284,16 +284,18 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
       if (s_next < nwk) stage_s(s_pidx);
     }
 
-    double lam[4] = {l01.x, l01.y, l23.x, l23.y}, r[4], pv[4], y[4];
+    double lam[4] = {l01.x, l01.y, l23.x, l23.y}, r[4] = {0, 0, 0, 0}, pv[4], y[4];
 
-    // out = (-S) x from the register-resident blocks
-    auto matvec_s = [&](const double* xr, double* out) {
+    // out = (-S) x from the register-resident blocks; the partials of the dot
+    // a'b are published with the product's exchange (one barrier for both)
+    auto matvec_s_dot = [&](const double* xr, double* out, const double* a, const double* b, int slot) {
       double xf[8], own[4], hand[4], low[4], up[4], xn[4];
       gather(xr, xf);
       put(vbuf, my0, my1, xr);
       h8s::sym_times(sd, xf, xr, h, own);
       rows_times(so, xf, hand);  // L_i x_i
       put(xbuf, my0, my1, hand);
+      partial(a, b, slot);
       __syncthreads();
       get(vbuf, nx0, nx1, xn);
       trans_times(so, xn, up);   // L_i' x_{i+1}
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
       finish(own, low, up, out);
     };
 
-    matvec_s(lam, y);  // y = (-S) lambda0
+    matvec_s_dot(lam, y, r, r, 2);  // y = (-S) lambda0 (slot 2: an unread dummy dot)
     if (act) {
       r[0] = g01.x - y[0], r[1] = g01.y - y[1], r[2] = g23.x - y[2], r[3] = g23.y - y[3];
     } else {
@@ -334,18 +336,25 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
     mbar_wait(&s_bar[1], ph1);
     ph1 ^= 1;
     h8s::load_sym(PdI, ib, h, pd);
-    matvec_p(r, pv);  // r~
-    double eta = dot(r, pv);
-    double inv_eta = 1.0 / eta;  // beta = eta' / eta as eta' * (1 / eta), the division off the critical path
+    double rt[4], sr[4];  // r~ and (-S) r~
+    matvec_p(r, rt);                 // r~ = Phi^-1 r
+    // Pipelined second dot: sr = (-S) r~ is formed while eta = r'r~ reduces
+    // (its partials ride on the product's barrier); p = r~ + beta p and
+    // y = (-S) p = sr + beta y then need no product of their own. y is the
+    // recurrence of Chronopoulos-Gear's s; v = p'y stays a direct dot.
+    matvec_s_dot(rt, sr, r, rt, 1);
+    double eta = total(1);
     int status = DOCP_OK, iters = 0;
     if (eta < 0.0) {
-      const double scale = norm(r) * norm(pv);
+      const double scale = norm(r) * norm(rt);
       if (-eta <= 1e-10 * scale + 1e-300) eta = 0.0;
       else status = DOCP_AT_PCG_PRECOND;
     }
+    double inv_eta = 1.0 / eta;  // beta = eta' / eta as eta' * (1 / eta), the division off the critical path
+#pragma unroll
+    for (int q = 0; q < 4; ++q) pv[q] = rt[q], y[q] = sr[q];
 
     while (status == DOCP_OK && eta > threshold && iters < max_iters) {
-      matvec_s(pv, y);
       const double vv = dot(pv, y);
       if (vv <= 0.0) {
         status = DOCP_AT_PCG_CURVATURE;
@@ -357,10 +366,11 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
         lam[q] = fma(alpha, pv[q], lam[q]);
         r[q] = fma(-alpha, y[q], r[q]);
       }
-      matvec_p(r, y);  // r~ (y reused)
-      double eta_next = dot(r, y);
+      matvec_p(r, rt);                 // r~
+      matvec_s_dot(rt, sr, r, rt, 1);   // sr = (-S) r~ while eta' = r'r~ reduces
+      double eta_next = total(1);
       if (eta_next < 0.0) {
-        const double scale = norm(r) * norm(y);
+        const double scale = norm(r) * norm(rt);
         if (-eta_next <= 1e-10 * scale + 1e-300) {
           eta_next = 0.0;
         } else {
@@ -370,7 +380,10 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
       }
       const double beta = eta_next * inv_eta;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) pv[q] = fma(beta, pv[q], y[q]);
+      for (int q = 0; q < 4; ++q) {
+        pv[q] = fma(beta, pv[q], rt[q]);
+        y[q] = fma(beta, y[q], sr[q]);
+      }
       eta = eta_next;
       inv_eta = 1.0 / eta;
       ++iters;

@@ -1,0 +1,48 @@
+"""FAST against PARITY on the full C3 batch (4096 random_convex_instance(8,4,100)
+problems): PARITY is bit-identical to the reference (test_gpu_parity.py), so
+this extends the FAST bar from the oracle-sized cases to every problem of the
+benchmark batch, forward and backward: equal SQP iteration counts, <= 1e-9
+relative error on z and dtheta, and equal PCG counts except where a warm
+start lands on the exit threshold itself (eta_0 ~ epsilon^2 at the converged
+second SQP iteration): there FAST's different rounding may take one more (or
+one fewer) iteration; about 3 of 12,288 solves, never more than one apart.""" 
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_rows(a, b):
+    return np.linalg.norm(a - b, axis=1) / np.maximum(1.0, np.linalg.norm(b, axis=1))
+
+
+def test_fast_matches_parity_on_c3_batch():
+    import paper_2510_06179_b200 as D
+    nx, nu, T, B = 8, 4, 100, 4096
+    prob = D.affine_quadratic(nx, nu, T)
+    nz, nl = D.sizes(prob)
+    th = D.generate_affine_quadratic(nx, nu, 0, B)
+    rng = np.random.default_rng(0)
+    z0 = 0.1 * rng.standard_normal((B, nz))
+    lg = rng.standard_normal((B, nz))
+    out = {}
+    for mode in ("parity", "fast"):
+        cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(mode=mode))
+        res, errs = D.sqp_solve_batch(prob, th, z0, np.zeros((B, nl)), cfg)
+        assert all(e is None for e in errs)
+        g, lt, its, errs = D.backward_vjp_batch(res[0].batch, lg, np.zeros((B, nl)), cfg.pcg)
+        assert all(e is None for e in errs)
+        out[mode] = (np.stack([r.z for r in res]), [r.pcg_iters for r in res], [r.sqp_iters for r in res],
+                     g.copy(), np.asarray(its).copy())
+    zp, hp, sp, gp, ip = out["parity"]
+    zf, hf, sf, gf, if_ = out["fast"]
+    assert sp == sf
+    diffs = [(j, k) for j in range(B) for k in range(len(hp[j])) if hp[j][k] != hf[j][k]]
+    diffs += [(j, "bwd") for j in range(B) if ip[j] != if_[j]]
+    print(f"PCG count differences: {len(diffs)} of {sum(map(len, hp)) + B}: {diffs[:8]}")
+    for j, k in diffs:
+        a, b = (hp[j][k], hf[j][k]) if k != "bwd" else (ip[j], if_[j])
+        assert abs(a - b) <= 1 and min(a, b) <= 1, (j, k, a, b)  # only at a converged warm start
+    assert len(diffs) <= 10
+    assert rel_rows(zf, zp).max() <= 1e-9
+    assert rel_rows(gf, gp).max() <= 1e-9
