@@ -4,15 +4,15 @@ OUT=gpurun_out
 tail -1 $OUT/plain.log | cut -c1-300
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/r1g_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_list.log 2>&1; echo "list rc=$?"
 export DOCP_PROFILE_RANGE=1
-for k in pcg_kernel_h8r assemble_kernel_t step_kernel kkt_kernel gamma_kernel recover_kernel vjp_kernel; do
+for k in pcg_kernel_h8s assemble_kernel_t step_kernel kkt_kernel gamma_kernel recover_kernel vjp_kernel; do
   timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:$k -c 1 \
      -o $OUT/r1g_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_$k.log 2>&1
   echo "$k rc=$?"
 done
 # summarise on the box (the reports themselves exceed gpurun's copy-back limit)
 python tools/ncu_summary.py $OUT/r1g_*.ncu-rep > $OUT/r1g_ncu_table.md
-python tools/ncu_summary.py --traffic $OUT/r1g_pcg_kernel_h8r.ncu-rep > $OUT/r1g_pcg_traffic.json
-for k in pcg_kernel_h8r assemble_kernel_t; do
+python tools/ncu_summary.py --traffic $OUT/r1g_pcg_kernel_h8s.ncu-rep > $OUT/r1g_pcg_traffic.json
+for k in pcg_kernel_h8s assemble_kernel_t; do
   ncu -i $OUT/r1g_$k.ncu-rep --page raw --csv > $OUT/r1g_${k}_raw.csv
   ncu -i $OUT/r1g_$k.ncu-rep --page source --csv --print-source cuda,sass > $OUT/r1g_${k}_src.csv
   python tools/ncu_lines.py $OUT/r1g_${k}_src.csv 40 > $OUT/r1g_${k}_lines.txt
