@@ -428,8 +428,11 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": D.describe(prob),
                          "algorithmic_bytes_per_iteration": prof["pcg_bytes_per_iteration"],
-                         "note": "blocks are SMEM-resident (TMA-staged once per solve), so algorithmic GB/s "
-                                 "exceeds HBM; binding roofline is SMEM",
+                         "note": "blocks are on-chip for the whole solve (diagonal blocks and -S sub blocks in "
+                                 "registers, Phi^-1 super blocks in SMEM, TMA-staged once per solve), so "
+                                 "algorithmic GB/s exceeds HBM (traffic = one record read per solve); "
+                                 "frac_smem compares with the derived SMEM ceiling; the iteration is "
+                                 "latency-bound (two reductions, four barriers)",
                          "smem_peak_derived": smem_peak, "frac_smem": achieved / smem_peak},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "problems/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

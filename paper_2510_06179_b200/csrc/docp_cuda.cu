@@ -1009,9 +1009,10 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   const bool res = pcg_smem(d, true) + 64 <= static_cast<size_t>(max_optin);
   const int cl = d.nx == 16 ? h16f_cluster_for(d, dev) : h8f_cluster_for(d, dev);
   const char* fk = d.nx == 16 ? "pcg_kernel_h16f" : "pcg_kernel_h8f";
-  char fast[64];
+  char fast[96];
   if (h4f_fits(d, dev)) snprintf(fast, sizeof fast, "pcg_kernel_h4f(resident)");
-  else if (cl == 1) snprintf(fast, sizeof fast, "%s(resident)", d.nx == 8 ? "pcg_kernel_h8r" : fk);
+  else if (cl == 1) snprintf(fast, sizeof fast, "%s(resident)",
+                           d.nx == 8 ? "pcg_kernel_h8s; uploaded systems pcg_kernel_h8r" : fk);
   else if (cl > 1) snprintf(fast, sizeof fast, "%s(cluster%d,resident)", fk, cl);
   else snprintf(fast, sizeof fast, "%s", d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
                                                    : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>");
