@@ -88,9 +88,9 @@ __global__ void init_solve_kernel(View v, int* __restrict__ list, int* __restric
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < v.B; p += warps) {
     const double* z = v.z + static_cast<long>(p) * d.nz;
     const double* l = v.lam + static_cast<long>(p) * d.nl;
-    bool fin = true;
-    for (int e = lane; e < d.nz; e += 32) fin = fin && isfinite(z[e]);
-    for (int e = lane; e < d.nl; e += 32) fin = fin && isfinite(l[e]);
+    bool fin = true;  // & (not &&): the loads are independent and stay in flight together
+    for (int e = lane; e < d.nz; e += 32) fin &= static_cast<bool>(isfinite(z[e]));
+    for (int e = lane; e < d.nl; e += 32) fin &= static_cast<bool>(isfinite(l[e]));
     fin = __all_sync(0xffffffffu, fin);
     if (lane == 0) {
       v.mu[p] = 1.0;
@@ -897,9 +897,11 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
     const int cols = 1 + learn_size;
     const int ctas = (cols + kIlSumThreads - 1) / kIlSumThreads;
     const int ncol = std::min(kIlSumThreads, cols);
-    const int rows = std::max(1, std::min(1024, (40 * 1024 / 8) / ncol));
-    il_sum_kernel<<<ctas, kIlSumThreads, static_cast<size_t>(rows) * ncol * sizeof(double), b->stream>>>(
-        b->v, learn_start, learn_size, rows, loss_sum, grad_sum);
+    // as few staging phases as 160 KB of shared memory allows
+    const int rows = std::max(1, std::min(b->B, (160 * 1024 / 8) / ncol - 1));
+    const size_t smem = static_cast<size_t>(rows | 1) * ncol * sizeof(double);
+    CUDA_TRY(cudaFuncSetAttribute(il_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    il_sum_kernel<<<ctas, kIlSumThreads, smem, b->stream>>>(b->v, learn_start, learn_size, rows, loss_sum, grad_sum);
   }
   LAUNCH_CHECK();
   return DOCP_OK;

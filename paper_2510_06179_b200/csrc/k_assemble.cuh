@@ -626,6 +626,14 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
         const double* lrt = lr + t * NU;
         const double* At = v.A + a_off(d, p, t);
         const double* Bt = v.Bm + b_off(d, p, t);
+        // FAST: the stage's cost diagonals are loaded first, so their latency
+        // overlaps the A / B staging below
+        double q_t = 0.0, q_n = 0.0, r_t = 0.0;
+        if constexpr (FAST) {
+          q_t = qdp[t * NX + l];
+          q_n = qdp[(t + 1) * NX + l];
+          if (l < NU) r_t = rdp[t * NU + l];
+        }
 #pragma unroll
         for (int k = l; k < B2; k += NX) sA[ix(k % NX, k / NX)] = At[k];
 #pragma unroll
@@ -634,12 +642,12 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
         // M1(k, l) = (A(l,k)/lq_k)/lq_k ; M2(k, l) = (B(l,k)/lr_k)/lr_k
         double c3;
         if constexpr (FAST) {  // lane k scales column k of A (of B) by 1/q_k (1/r_k)
-          dq = __drcp_rn(qdp[t * NX + l]);
-          c3 = __drcp_rn(qdp[(t + 1) * NX + l]);
+          dq = __drcp_rn(q_t);
+          c3 = __drcp_rn(q_n);
 #pragma unroll
           for (int j = 0; j < NX; ++j) sM1[ix(l, j)] = sA[ix(j, l)] * dq;
           if (l < NU) {
-            const double ir = __drcp_rn(rdp[t * NU + l]);
+            const double ir = __drcp_rn(r_t);
 #pragma unroll
             for (int j = 0; j < NX; ++j) sM2[iu(l, j)] = sB[ix(j, l)] * ir;
           }

@@ -18,7 +18,7 @@
 
 namespace docp_dev {
 
-constexpr int kStepThreads = 256;
+constexpr int kStepThreads = 128;
 
 struct StepCfg {
   int n_alpha;
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
 /// stage. NX, NU > 0 fix the block sizes at compile time.
 constexpr int kKktThreads = 128;
 template <int NX, int NU>
-__global__ void __launch_bounds__(kKktThreads) kkt_kernel(View v, const int* __restrict__ work,
+__global__ void __launch_bounds__(kKktThreads, 4) kkt_kernel(View v, const int* __restrict__ work,
                                                         const int* __restrict__ n_work) {
   extern __shared__ double sm_kkt[];
   __shared__ unsigned long long s_max;
@@ -503,23 +503,25 @@ constexpr int kIlSumThreads = 256;
 __global__ void __launch_bounds__(kIlSumThreads) il_sum_kernel(View v, int learn_start, int learn_size, int rows,
                                                                double* __restrict__ loss_sum,
                                                                double* __restrict__ grad_sum) {
-  extern __shared__ double stage_buf[];  // [rows][ncol]
+  extern __shared__ double stage_buf[];  // [ncol][ld]: column-major, odd leading dimension
   const int c0 = blockIdx.x * kIlSumThreads;
   const int ncol = min(kIlSumThreads, 1 + learn_size - c0);
+  const int ld = rows | 1;  // the folding threads walk their columns on distinct banks
   const int k = threadIdx.x;
   double acc = 0.0;
   for (int p0 = 0; p0 < v.B; p0 += rows) {
     const int n = min(rows, v.B - p0);
     __syncthreads();
     for (int g = threadIdx.x; g < n * ncol; g += blockDim.x) {
-      const int j = g / ncol, c = c0 + (g - j * ncol);
+      const int j = g / ncol, c = g - j * ncol;
       const long p = p0 + j;
-      stage_buf[g] = c == 0 ? v.loss[p] : v.grad[p * v.d.nth + learn_start + c - 1];
+      stage_buf[c * ld + j] = c0 + c == 0 ? v.loss[p] : v.grad[p * v.d.nth + learn_start + c0 + c - 1];
     }
     __syncthreads();
     if (k < ncol) {
+      const double* col = stage_buf + k * ld;
 #pragma unroll 8
-      for (int j = 0; j < n; ++j) acc = acc + stage_buf[j * ncol + k];
+      for (int j = 0; j < n; ++j) acc = acc + col[j];  // instance order (train.hpp:126-131)
     }
   }
   if (k < ncol) {
