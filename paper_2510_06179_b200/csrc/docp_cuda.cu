@@ -1011,8 +1011,11 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   const bool res = pcg_smem(d, true) + 64 <= static_cast<size_t>(max_optin);
   const int cl = d.nx == 16 ? h16f_cluster_for(d, dev) : h8f_cluster_for(d, dev);
   const char* fk = d.nx == 16 ? "pcg_kernel_h16f" : "pcg_kernel_h8f";
-  char fast[96];
+  char fast[128];
+  const int s8 = d.nx == 8 ? h8s_variant_for(d, dev) : 0;
   if (h4f_fits(d, dev)) snprintf(fast, sizeof fast, "pcg_kernel_h4f(resident)");
+  else if (s8 >= 2) snprintf(fast, sizeof fast, "pcg_kernel_h8s<%d,no-prefetch>(resident); uploaded systems %s",
+                             s8 == 2 ? 256 : 288, cl == 2 ? "pcg_kernel_h8f(cluster2)" : "pcg_kernel_h8f");
   else if (cl == 1) snprintf(fast, sizeof fast, "%s(resident)",
                            d.nx == 8 ? "pcg_kernel_h8s; uploaded systems pcg_kernel_h8r" : fk);
   else if (cl > 1) snprintf(fast, sizeof fast, "%s(cluster%d,resident)", fk, cl);

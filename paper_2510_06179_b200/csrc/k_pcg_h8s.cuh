@@ -80,11 +80,23 @@ __device__ __forceinline__ void sym_times(const Sym& m, const double* xf, const 
 
 }  // namespace h8s
 
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __restrict__ work,
-                                                        const int* __restrict__ n_work, int* __restrict__ counter,
-                                                        double* __restrict__ sol_all, double epsilon,
-                                                        int max_iters_cfg) {
+/// Dynamic shared memory of pcg_kernel_h8s (doubles). PREFETCH: Phi^-1 of the
+/// current problem plus a staging area for the next problem's -S; otherwise
+/// one record-sized region that takes -S, then Phi^-1, of the current problem.
+template <int MAXT, bool PREFETCH>
+__host__ __device__ inline long h8s_smem_doubles(const Dims& d) {
+  constexpr int NWS = MAXT <= 256 ? 8 : 16;
+  return (PREFETCH ? 4L : 2L) * d.nb * 64 + 2L * (d.nb + 2) * 8 + 3 * NWS;
+}
+
+/// MAXT = 256: 255 registers per thread; with PREFETCH = false (T <= 127) the
+/// -S and Phi^-1 halves of a record that does not fit twice in shared memory
+/// are loaded one after the other into the same region. pcg_kernel_h8s_288
+/// (below) extends that to T <= 143.
+template <int MAXT, bool PREFETCH>
+__device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, const int* __restrict__ n_work,
+                                         int* __restrict__ counter, double* __restrict__ sol_all, double epsilon,
+                                         int max_iters_cfg) {
   extern __shared__ __align__(128) double sm_pcg[];
   __shared__ __align__(8) uint64_t s_bar[2];  // [0]: staged -S blocks, [1]: Phi^-1 blocks
   __shared__ int s_next, s_pidx;
@@ -100,13 +112,16 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
   const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int nwk = *n_work;
 
+  constexpr int NWS = MAXT <= 256 ? 8 : 16;  // warp slots per dot
   double* sPd = sm_pcg;            // [R] Phi^-1 diagonal blocks (current problem)
   double* sPu = sPd + R * 64;      // [R] Phi^-1 super blocks
-  double* sNd = sPu + R * 64;      // [R] -S diagonal blocks (next problem, staging)
-  double* sNs = sNd + R * 64;      // [R] -S sub blocks
-  double* vbuf = sNs + R * 64;     // [R + 2] x_i halves (slot = row + 1)
+  // -S diagonal / sub blocks: the next problem's (staging) or, without the
+  // prefetch, the current problem's in the same region as Phi^-1
+  double* sNd = PREFETCH ? sPu + R * 64 : sPd;
+  double* sNs = sNd + R * 64;
+  double* vbuf = sPu + (PREFETCH ? 3 : 1) * R * 64;  // [R + 2] x_i halves (slot = row + 1)
   double* xbuf = vbuf + (R + 2) * 8;
-  double* red = xbuf + (R + 2) * 8;  // [3][8] dot partials
+  double* red = xbuf + (R + 2) * 8;  // [3][NWS] dot partials
 
   const int p = i & 1, m = (i >> 1) & 1;
   h8f::Bases bs;
@@ -145,12 +160,12 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
     if (bo) tma_bulk_g2s(sNs, rec + d.s_sub, bo, &s_bar[0]);
   };
 
-  if (tid < 24) red[tid] = 0.0;
+  if (tid < 3 * NWS) red[tid] = 0.0;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     grab();
-    if (s_next < nwk) stage_s(s_pidx);
+    if (PREFETCH && s_next < nwk) stage_s(s_pidx);
   }
   __syncthreads();
   uint32_t phase = 0, ph1 = 0;  // parities of s_bar[0] (staging) and s_bar[1] (Phi^-1)
@@ -161,13 +176,19 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
     double s = fma(a[3], b[3], fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0])));
     s = act ? s : 0.0;
     s = warp_sum(s);
-    if (lane == 0) red[slot * 8 + warp] = s;
+    if (lane == 0) red[slot * NWS + warp] = s;
   };
   // pairwise over the 8 warp slots (slots of absent warps hold 0): depth 3
   auto total = [&](int slot) -> double {
-    const double2* q = reinterpret_cast<const double2*>(red + slot * 8);
+    const double2* q = reinterpret_cast<const double2*>(red + slot * NWS);
     const double2 a = q[0], b = q[1], c = q[2], e = q[3];
-    return ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (e.x + e.y));
+    const double t8 = ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (e.x + e.y));
+    if constexpr (NWS == 8) {
+      return t8;
+    } else {
+      const double2 f = q[4], g = q[5], k = q[6], m = q[7];
+      return t8 + (((f.x + f.y) + (g.x + g.y)) + ((k.x + k.y) + (m.x + m.y)));
+    }
   };
   auto dot = [&](const double* a, const double* b) -> double {
     partial(a, b, 0);
@@ -260,19 +281,33 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
       g23 = *reinterpret_cast<const double2*>(gam + i * 8 + 4 * h + 2);
     }
     const bool runnable = v.status[pidx].code == DOCP_OK;  // failed in an earlier stage: skip
+    if constexpr (!PREFETCH) {
+      if (!runnable) {  // block-uniform
+        __syncthreads();  // s_next / s_pidx read by every thread
+        if (tid == 0) grab();
+        __syncthreads();
+        continue;
+      }
+      if (tid == 0) {  // this problem's -S into the record region (free since the last barrier)
+        fence_proxy_async();
+        stage_s(pidx);
+      }
+    }
     mbar_wait(&s_bar[0], phase);
     h8s::load_sym(NdI, ib, h, sd);
     h8f::load_rows(NsI, bs, so);
     __syncthreads();  // staging area consumed; s_next / s_pidx read; Phi^-1 reads of the previous problem done
     phase ^= 1;
-    if (!runnable) {  // block-uniform; s_bar[1] is not armed for a skipped problem
-      if (tid == 0) {
-        fence_proxy_async();
-        grab();
-        if (s_next < nwk) stage_s(s_pidx);
+    if constexpr (PREFETCH) {
+      if (!runnable) {  // block-uniform; s_bar[1] is not armed for a skipped problem
+        if (tid == 0) {
+          fence_proxy_async();
+          grab();
+          if (s_next < nwk) stage_s(s_pidx);
+        }
+        __syncthreads();
+        continue;
       }
-      __syncthreads();
-      continue;
     }
     if (tid == 0) {
       fence_proxy_async();
@@ -281,7 +316,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
       tma_bulk_g2s(sPd, rec + d.p_diag, bd, &s_bar[1]);
       if (bo) tma_bulk_g2s(sPu, rec + d.p_sup, bo, &s_bar[1]);
       grab();  // s_next / s_pidx: read after the end-of-problem barrier
-      if (s_next < nwk) stage_s(s_pidx);
+      if (PREFETCH && s_next < nwk) stage_s(s_pidx);
     }
 
     double lam[4] = {l01.x, l01.y, l23.x, l23.y}, r[4] = {0, 0, 0, 0}, pv[4], y[4];
@@ -405,6 +440,22 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
     }
     __syncthreads();  // s_next is published; Phi^-1 / vectors free for the next problem
   }
+}
+
+template <int MAXT, bool PREFETCH>
+__global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __restrict__ work,
+                                                        const int* __restrict__ n_work, int* __restrict__ counter,
+                                                        double* __restrict__ sol_all, double epsilon,
+                                                        int max_iters_cfg) {
+  h8s_body<MAXT, PREFETCH>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
+}
+
+/// 288 threads (T <= 143): nine warps, so one SMSP holds three of them and its
+/// quarter of the register file (16K) caps every thread at 168 registers.
+__global__ void __maxnreg__(168)
+    pcg_kernel_h8s_288(View v, const int* __restrict__ work, const int* __restrict__ n_work,
+                       int* __restrict__ counter, double* __restrict__ sol_all, double epsilon, int max_iters_cfg) {
+  h8s_body<288, false>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
 }
 
 }  // namespace docp_dev

@@ -87,22 +87,42 @@ static int launch_h8r(docp_batch* b, const int* list, const int* count, int n_hi
 }
 
 /// FAST, one CTA per problem, device-assembled (symmetric) diagonal blocks:
-/// pcg_kernel_h8s (both diagonal blocks in registers).
+/// pcg_kernel_h8s (both diagonal blocks in registers). Returns -1 (nothing
+/// launched) when the variant does not fit this shape.
+template <int MAXT, bool PREFETCH>
 static int launch_h8s(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
                       int max_iters) {
-  auto kern = pcg_kernel_h8s<256>;
-  const size_t smem = h8r_smem_doubles(b->d) * sizeof(double);
+  auto kern = MAXT == 288 ? pcg_kernel_h8s_288 : pcg_kernel_h8s<MAXT, PREFETCH>;
   const int threads = (2 * b->d.nb + 31) / 32 * 32;
+  if (threads > MAXT) return -1;
+  const size_t smem = h8s_smem_doubles<MAXT, PREFETCH>(b->d) * sizeof(double);
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device);
+  if (smem + 256 > static_cast<size_t>(max_optin)) return -1;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg: kernel does not fit on an SM (smem %zu)", smem);
+  if (per_sm < 1) return -1;
   const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
   CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
   ProfScope ps(b, DOCP_PROF_PCG);
   kern<<<grid, threads, smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
   LAUNCH_CHECK();
   return DOCP_OK;
+}
+
+/// The h8s variant for this shape (0: none): 1 = prefetching, 256 threads
+/// (T <= 113); 2 = no prefetch, 256 threads (T <= 127); 3 = no prefetch, 288
+/// threads at 168 registers (T <= 143).
+int h8s_variant_for(const Dims& d, int device) {
+  if (d.nx != 8) return 0;
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  const int threads = (2 * d.nb + 31) / 32 * 32;
+  if (threads <= 256 && h8s_smem_doubles<256, true>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 1;
+  if (threads <= 256 && h8s_smem_doubles<256, false>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 2;
+  if (threads <= 288 && h8s_smem_doubles<288, false>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 3;
+  return 0;
 }
 
 /// Smallest cluster (1, 2, 4, 8) whose per-CTA share of the blocks fits in
@@ -134,11 +154,20 @@ static bool force_h8() { return force_variant("h8"); }
 /// blocks on-chip; PARITY (or no fitting cluster): two threads per block row
 /// (pcg_kernel_h8) up to T = 255, one thread per block row (pcg_kernel) beyond.
 DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
+  if (!par && !force_h8() && b->sym_blocks && !force_variant("h8r") && !force_variant("h8f")) {
+    int rc = -1;
+    switch (h8s_variant_for(b->d, b->device)) {
+      case 1: rc = launch_h8s<256, true>(b, list, count, n_hint, sol, eps, max_iters); break;
+      case 2: rc = launch_h8s<256, false>(b, list, count, n_hint, sol, eps, max_iters); break;
+      case 3: rc = launch_h8s<288, false>(b, list, count, n_hint, sol, eps, max_iters); break;
+      default: break;
+    }
+    if (rc != -1) return rc;
+  }
   if (!par && !force_h8()) {
     switch (h8f_cluster(b)) {
       case 1:
         if (force_variant("h8f")) return launch_h8f_cl<1>(b, list, count, n_hint, sol, eps, max_iters);
-        if (b->sym_blocks && !force_variant("h8r")) return launch_h8s(b, list, count, n_hint, sol, eps, max_iters);
         return launch_h8r(b, list, count, n_hint, sol, eps, max_iters);
       case 2: return launch_h8f_cl<2>(b, list, count, n_hint, sol, eps, max_iters);
       case 4: return launch_h8f_cl<4>(b, list, count, n_hint, sol, eps, max_iters);

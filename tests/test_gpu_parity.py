@@ -276,7 +276,7 @@ def _oracle_solve_and_grad(pprob, th, z0, lam0, cfg_port, lg, lt0):
 
 @pytest.mark.parametrize("mode", ["parity", "fast"])
 @pytest.mark.parametrize("nx,nu,T,seed,max_it", [(4, 2, 20, 11, 20), (8, 4, 30, 12, 20), (8, 4, 100, 13, 5),
-                                                 (3, 2, 4, 14, 20), (16, 8, 30, 15, 20)])
+                                                 (8, 4, 127, 16, 5), (3, 2, 4, 14, 20), (16, 8, 30, 15, 20)])
 def test_sqp_backward_affine_quadratic(D, mode, nx, nu, T, seed, max_it):
     B = 4
     th = aq_thetas(nx, nu, T, seed, B)
@@ -562,13 +562,17 @@ def test_pcg_breakdown_all_kernels(D, nx, nu, T):
         assert b.download(D._lib.F_PCG_ITERS)[1, 0] == want_ok[1]
 
 
-@pytest.mark.parametrize("nx,nu,T", [(8, 4, 1), (8, 4, 2), (8, 4, 30), (8, 4, 100), (8, 4, 113)])
+@pytest.mark.parametrize("nx,nu,T", [(8, 4, 1), (8, 4, 2), (8, 4, 30), (8, 4, 100), (8, 4, 113), (8, 4, 120),
+                                     (8, 4, 127), (8, 4, 128), (8, 4, 143)])
 def test_fast_nx8_kernels_agree(D, nx, nu, T, monkeypatch):
     """The n_x = 8 single-CTA FAST kernels: pcg_kernel_h8r (-S in registers)
     and pcg_kernel_h8f fold every sum in the same order and agree bit for bit;
     pcg_kernel_h8s (the default for device-assembled systems: both symmetric
-    diagonal blocks packed in registers) folds the diagonal products in
+    diagonal blocks packed in registers; T > 113: the 288-thread form without
+    the prefetch, against the h8f cluster) folds the diagonal products in
     another order: same iteration counts, iterates within 1e-12."""
+    if T > 113:
+        assert "no-prefetch" in D.describe(D.affine_quadratic(nx, nu, T))
     th = aq_thetas(nx, nu, T, 77, 5)
     b = D.Batch(D.affine_quadratic(nx, nu, T), 5)
     b.upload(D._lib.F_THETA, th)
