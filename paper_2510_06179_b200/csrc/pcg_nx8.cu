@@ -156,7 +156,9 @@ static bool force_h8() { return force_variant("h8"); }
 DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
   if (!par && !force_h8() && b->sym_blocks && !force_variant("h8r") && !force_variant("h8f")) {
     int rc = -1;
-    switch (h8s_variant_for(b->d, b->device)) {
+    int var = h8s_variant_for(b->d, b->device);
+    if (var == 1 && force_variant("h8s_np")) var = 2;  // A/B: the no-prefetch form on a short horizon
+    switch (var) {
       case 1: rc = launch_h8s<256, true>(b, list, count, n_hint, sol, eps, max_iters); break;
       case 2: rc = launch_h8s<256, false>(b, list, count, n_hint, sol, eps, max_iters); break;
       case 3: rc = launch_h8s<288, false>(b, list, count, n_hint, sol, eps, max_iters); break;
