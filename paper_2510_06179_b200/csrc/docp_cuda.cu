@@ -893,7 +893,9 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
   il_loss_kernel<<<grid_for(static_cast<long>(b->B) * 32, kIlLossThreads, b->num_sms * 8), kIlLossThreads, 0, b->stream>>>(b->v, demos, den);
   LAUNCH_CHECK();
   if ((rc = docp_backward_vjp(b, &cfg->pcg))) return rc;
-  {
+  if (cfg->pcg.mode == DOCP_PCG_FAST) {
+    il_sum_tree_kernel<<<1 + learn_size, kIlTreeThreads, 0, b->stream>>>(b->v, learn_start, loss_sum, grad_sum);
+  } else {
     const int cols = 1 + learn_size;
     const int ctas = (cols + kIlSumThreads - 1) / kIlSumThreads;
     const int ncol = std::min(kIlSumThreads, cols);

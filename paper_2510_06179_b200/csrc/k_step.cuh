@@ -530,4 +530,30 @@ __global__ void __launch_bounds__(kIlSumThreads) il_sum_kernel(View v, int learn
   }
 }
 
+/// FAST mode: the same sums as il_sum_kernel, as a fixed-shape tree (one CTA
+/// per column: strided per-thread sums, then a warp tree and a pairwise sum
+/// of the warp partials). Deterministic; it differs from the instance-order
+/// fold only by rounding, so PARITY keeps il_sum_kernel.
+constexpr int kIlTreeThreads = 1024;
+__global__ void __launch_bounds__(kIlTreeThreads) il_sum_tree_kernel(View v, int learn_start,
+                                                                     double* __restrict__ loss_sum,
+                                                                     double* __restrict__ grad_sum) {
+  __shared__ double part[kIlTreeThreads / 32];
+  const int c = blockIdx.x;  // 0: loss, 1 + k: learnable gradient k
+  double acc = 0.0;
+  for (int p = threadIdx.x; p < v.B; p += blockDim.x)
+    acc += c == 0 ? v.loss[p] : v.grad[static_cast<long>(p) * v.d.nth + learn_start + c - 1];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = part[threadIdx.x];
+    t = warp_sum(t);
+    if (threadIdx.x == 0) {
+      if (c == 0) *loss_sum = t;
+      else grad_sum[c - 1] = t;
+    }
+  }
+}
+
 }  // namespace docp_dev
