@@ -334,6 +334,19 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       phase2(precond, oo, vbuf, xbuf, low, up);
       finish(own, low, up, out);
     };
+    // (-S) x with the partials of the dot a'b published before the product's
+    // (cluster) barrier, which then serves both
+    auto matvec_s_dot = [&](const double* xr, double* out, const double* a, const double* b, int slot) {
+      double2 dd[8][2], oo[8][2];
+      h8f::load_rows(SdI, bs, dd);
+      h8f::load_rows(SsI, bs, oo);
+      double own[4], low[4], up[4];
+      phase1(false, dd, oo, xr, vbuf, xbuf, own);
+      partial(a, b, slot);
+      h8f_sync<CL>();
+      phase2(false, oo, vbuf, xbuf, low, up);
+      finish(own, low, up, out);
+    };
 
     matvec(false, lam, y);  // y = (-S) lambda0
     if (act) {
@@ -347,14 +360,15 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
     mbar_wait(&s_bar[1], phase);
     phase ^= 1;
     matvec(true, r, pv);  // r~
-    double eta = dot(r, pv);
     int status = DOCP_OK, iters = 0;
+    double finals_eta = 0.0;
+    if constexpr (CL == 1) {  // the single-CTA form folds exactly as pcg_kernel_h8r
+    double eta = dot(r, pv);
     if (eta < 0.0) {
       const double scale = norm(r) * norm(pv);
       if (-eta <= 1e-10 * scale + 1e-300) eta = 0.0;
       else status = DOCP_AT_PCG_PRECOND;
     }
-
     while (status == DOCP_OK && eta > threshold && iters < max_iters) {
       matvec(false, pv, y);
       const double vv = dot(pv, y);
@@ -386,14 +400,67 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       ++iters;
     }
 
+    finals_eta = eta;
+    } else {
+    // Clusters: the second dot is pipelined as in pcg_kernel_h8s: w = (-S) r~
+    // is formed while eta' = r'r~ reduces (one cluster barrier fewer per
+    // iteration), p = r~ + beta p, y = w + beta y (Chronopoulos-Gear's s).
+    double rt[4], sr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rt[q] = pv[q];
+    matvec_s_dot(rt, sr, r, rt, 1);
+    double eta = total(1);
+    if (eta < 0.0) {
+      const double scale = norm(r) * norm(rt);
+      if (-eta <= 1e-10 * scale + 1e-300) eta = 0.0;
+      else status = DOCP_AT_PCG_PRECOND;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) y[q] = sr[q];
+    while (status == DOCP_OK && eta > threshold && iters < max_iters) {
+      const double vv = dot(pv, y);
+      if (vv <= 0.0) {
+        status = DOCP_AT_PCG_CURVATURE;
+        break;
+      }
+      const double alpha = eta / vv;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        lam[q] = fma(alpha, pv[q], lam[q]);
+        r[q] = fma(-alpha, y[q], r[q]);
+      }
+      matvec(true, r, rt);               // r~
+      matvec_s_dot(rt, sr, r, rt, 1);    // (-S) r~ while eta' = r'r~ reduces
+      double eta_next = total(1);
+      if (eta_next < 0.0) {
+        const double scale = norm(r) * norm(rt);
+        if (-eta_next <= 1e-10 * scale + 1e-300) {
+          eta_next = 0.0;
+        } else {
+          status = DOCP_AT_PCG_PRECOND;
+          break;
+        }
+      }
+      const double beta = eta_next / eta;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pv[q] = fma(beta, pv[q], rt[q]);
+        y[q] = fma(beta, y[q], sr[q]);
+      }
+      eta = eta_next;
+      ++iters;
+    }
+    finals_eta = eta;
+    }
+
     if (act) {
       *reinterpret_cast<double2*>(sol + i * 8 + 4 * h) = make_double2(lam[0], lam[1]);
       *reinterpret_cast<double2*>(sol + i * 8 + 4 * h + 2) = make_double2(lam[2], lam[3]);
     }
     if (tid == 0 && crank == 0) {
       v.pcg_iters[pidx] = iters;
-      v.final_eta[pidx] = eta;
-      v.pcg_conv[pidx] = status == DOCP_OK && eta <= threshold;
+      v.final_eta[pidx] = finals_eta;
+      v.pcg_conv[pidx] = status == DOCP_OK && finals_eta <= threshold;
       if (status == DOCP_OK) set_status(v.status + pidx, DOCP_OK, DOCP_AT_NONE, 0);
       else set_status(v.status + pidx, DOCP_BREAKDOWN, status, iters);
       atomicAdd(v.pcg_acc, static_cast<unsigned long long>(iters));
