@@ -91,8 +91,8 @@ __host__ __device__ inline long h8s_smem_doubles(const Dims& d) {
 
 /// MAXT = 256: 255 registers per thread; with PREFETCH = false (T <= 127) the
 /// -S and Phi^-1 halves of a record that does not fit twice in shared memory
-/// are loaded one after the other into the same region. pcg_kernel_h8s_288
-/// (below) extends that to T <= 143.
+/// are loaded one after the other into the same region. pcg_kernel_h8s_wide
+/// (below) extends that to T <= 191.
 template <int MAXT, bool PREFETCH>
 __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, const int* __restrict__ n_work,
                                          int* __restrict__ counter, double* __restrict__ sol_all, double epsilon,
@@ -450,12 +450,13 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
   h8s_body<MAXT, PREFETCH>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
 }
 
-/// 288 threads (T <= 143): nine warps, so one SMSP holds three of them and its
-/// quarter of the register file (16K) caps every thread at 168 registers.
+/// Up to 384 threads (T <= 191): 9-12 warps, so an SMSP holds three of them
+/// and its quarter of the register file (16K) caps every thread at 168
+/// registers (some spilling).
 __global__ void __maxnreg__(168)
-    pcg_kernel_h8s_288(View v, const int* __restrict__ work, const int* __restrict__ n_work,
-                       int* __restrict__ counter, double* __restrict__ sol_all, double epsilon, int max_iters_cfg) {
-  h8s_body<288, false>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
+    pcg_kernel_h8s_wide(View v, const int* __restrict__ work, const int* __restrict__ n_work,
+                        int* __restrict__ counter, double* __restrict__ sol_all, double epsilon, int max_iters_cfg) {
+  h8s_body<384, false>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
 }
 
 }  // namespace docp_dev

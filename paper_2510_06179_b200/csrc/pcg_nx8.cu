@@ -92,7 +92,7 @@ static int launch_h8r(docp_batch* b, const int* list, const int* count, int n_hi
 template <int MAXT, bool PREFETCH>
 static int launch_h8s(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
                       int max_iters) {
-  auto kern = MAXT == 288 ? pcg_kernel_h8s_288 : pcg_kernel_h8s<MAXT, PREFETCH>;
+  auto kern = MAXT == 384 ? pcg_kernel_h8s_wide : pcg_kernel_h8s<MAXT, PREFETCH>;
   const int threads = (2 * b->d.nb + 31) / 32 * 32;
   if (threads > MAXT) return -1;
   const size_t smem = h8s_smem_doubles<MAXT, PREFETCH>(b->d) * sizeof(double);
@@ -112,8 +112,8 @@ static int launch_h8s(docp_batch* b, const int* list, const int* count, int n_hi
 }
 
 /// The h8s variant for this shape (0: none): 1 = prefetching, 256 threads
-/// (T <= 113); 2 = no prefetch, 256 threads (T <= 127); 3 = no prefetch, 288
-/// threads at 168 registers (T <= 143).
+/// (T <= 113); 2 = no prefetch, 256 threads (T <= 127); 3 = no prefetch, up
+/// to 384 threads at 168 registers (T <= 191).
 int h8s_variant_for(const Dims& d, int device) {
   if (d.nx != 8) return 0;
   int max_optin = 0;
@@ -121,7 +121,7 @@ int h8s_variant_for(const Dims& d, int device) {
   const int threads = (2 * d.nb + 31) / 32 * 32;
   if (threads <= 256 && h8s_smem_doubles<256, true>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 1;
   if (threads <= 256 && h8s_smem_doubles<256, false>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 2;
-  if (threads <= 288 && h8s_smem_doubles<288, false>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 3;
+  if (threads <= 384 && h8s_smem_doubles<384, false>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 3;
   return 0;
 }
 
@@ -161,7 +161,7 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
     switch (var) {
       case 1: rc = launch_h8s<256, true>(b, list, count, n_hint, sol, eps, max_iters); break;
       case 2: rc = launch_h8s<256, false>(b, list, count, n_hint, sol, eps, max_iters); break;
-      case 3: rc = launch_h8s<288, false>(b, list, count, n_hint, sol, eps, max_iters); break;
+      case 3: rc = launch_h8s<384, false>(b, list, count, n_hint, sol, eps, max_iters); break;
       default: break;
     }
     if (rc != -1) return rc;
