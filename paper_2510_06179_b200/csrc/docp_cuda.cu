@@ -890,7 +890,11 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
                     b->stream>>>(b->v, weights, learn_start, learn_size, demos);
   LAUNCH_CHECK();
   if ((rc = docp_sqp_solve(b, cfg))) return rc;
-  il_loss_kernel<<<grid_for(static_cast<long>(b->B) * 32, kIlLossThreads, b->num_sms * 8), kIlLossThreads, 0, b->stream>>>(b->v, demos, den);
+  {
+    auto kl = cfg->pcg.mode == DOCP_PCG_FAST ? il_loss_kernel<true> : il_loss_kernel<false>;
+    kl<<<grid_for(static_cast<long>(b->B) * 32, kIlLossThreads, b->num_sms * 8), kIlLossThreads, 0, b->stream>>>(
+        b->v, demos, den);
+  }
   LAUNCH_CHECK();
   if ((rc = docp_backward_vjp(b, &cfg->pcg))) return rc;
   if (cfg->pcg.mode == DOCP_PCG_FAST) {

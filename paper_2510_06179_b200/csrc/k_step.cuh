@@ -456,6 +456,9 @@ __global__ void il_setup_kernel(View v, const double* __restrict__ weights, int 
 /// memory and lane 0 folds them in (t, i) order, as the reference does.
 constexpr int kIlLossThreads = 256;
 constexpr int kIlLossChunk = 256;  // staged squares per warp per pass
+/// FAST = true: every lane accumulates its own squares and the warp sums
+/// them as a tree (same value up to rounding; PARITY folds in (t, i) order).
+template <bool FAST>
 __global__ void __launch_bounds__(kIlLossThreads) il_loss_kernel(View v, const double* __restrict__ demos, double den) {
   __shared__ double sq[kIlLossThreads / 32][kIlLossChunk];
   const Dims d = v.d;
@@ -477,11 +480,13 @@ __global__ void __launch_bounds__(kIlLossThreads) il_loss_kernel(View v, const d
         double gv = 0.0;
         if (r >= d.nx && t < d.T) {
           const double du = z[e] - dm[e];
-          sq[w][(t * d.nu + r - d.nx) - (base / stage) * d.nu] = du * du;
+          if constexpr (FAST) acc += du * du;
+          else sq[w][(t * d.nu + r - d.nx) - (base / stage) * d.nu] = du * du;
           gv = g2 * du;
         }
         lg[e] = gv;
       }
+      if constexpr (FAST) continue;
       __syncwarp();
       if (lane == 0) {
         const int k0 = (base / stage) * d.nu;
@@ -490,6 +495,7 @@ __global__ void __launch_bounds__(kIlLossThreads) il_loss_kernel(View v, const d
       }
       __syncwarp();
     }
+    if constexpr (FAST) acc = warp_sum(acc);
     if (lane == 0) v.loss[p] = acc / den;
   }
 }
