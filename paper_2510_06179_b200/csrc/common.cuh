@@ -201,6 +201,32 @@ __device__ inline void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, 
 
 __device__ inline void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+/// Coalesced global -> shared staging by the whole CTA: src[e] goes to
+/// dst[map(e)]. Each thread issues U loads before their stores, so U loads
+/// are in flight per thread; a plain copy loop leaves one, since the
+/// compiler cannot move a load above the previous store through the generic
+/// shared-memory pointer.
+template <int U = 8, class Map>
+__device__ __forceinline__ void cta_stage(double* dst, const double* __restrict__ src, int n, Map map) {
+  for (int e0 = threadIdx.x; e0 < n; e0 += U * blockDim.x) {
+    double t[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int e = e0 + k * blockDim.x;
+      t[k] = e < n ? src[e] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int e = e0 + k * blockDim.x;
+      if (e < n) dst[map(e)] = t[k];
+    }
+  }
+}
+template <int U = 8>
+__device__ __forceinline__ void cta_stage(double* dst, const double* __restrict__ src, int n) {
+  cta_stage<U>(dst, src, n, [](int e) { return e; });
+}
+
 __device__ inline double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -195,8 +195,8 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
   const double* th = v.theta + static_cast<long>(p) * d.nth;
   const double* z = v.z + static_cast<long>(p) * d.nz;
   if (stage) {  // made visible by the __syncthreads below
-    for (int e = tid; e < d.nz; e += blockDim.x) stage[e] = z[e];
-    for (int e = tid; e < d.nth; e += blockDim.x) stage[d.nz + e] = th[e];
+    cta_stage(stage, z, d.nz);
+    cta_stage(stage + d.nz, th, d.nth);
     z = stage;
     th = stage + d.nz;
   }
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(128) recover_kernel(View v, const int* __restr
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
     const double* lamg = lam_all + static_cast<long>(p) * nl;
-    for (int e = threadIdx.x; e < nl; e += blockDim.x) sm_rec[e] = lamg[e];
+    cta_stage(sm_rec, lamg, nl);
     __syncthreads();
     const double* lam = sm_rec;
     const double* lg = v.lgz + static_cast<long>(p) * nz;

@@ -140,12 +140,13 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
     if constexpr (STAGE) {
       const double* th = v.theta + static_cast<long>(p) * d.nth;
       const double* zq = v.zqp + static_cast<long>(p) * d.nz;
-      for (int e = tid; e < d.nz; e += blockDim.x) {
-        const int t = e / (nx + nu), c = e - t * (nx + nu);
-        szo[t * P + c] = zo[e];
-        szq[t * P + c] = zq[e];
-      }
-      for (int e = tid; e < d.nth; e += blockDim.x) sth[e] = th[e];
+      auto padded = [&](int e) {
+        const int t = e / (nx + nu);
+        return t * P + (e - t * (nx + nu));
+      };
+      cta_stage<4>(szo, zo, d.nz, padded);
+      cta_stage<4>(szq, zq, d.nz, padded);
+      cta_stage(sth, th, d.nth);
     } else {  // the flat layout has the same stage stride: read in place
       szo = zo;
       szq = v.zqp + static_cast<long>(p) * d.nz;
@@ -304,13 +305,12 @@ __global__ void __launch_bounds__(kKktThreads, 4) kkt_kernel(View v, const int* 
     const int p = work[w];
     if (v.status[p].code != DOCP_OK) continue;
     if (threadIdx.x == 0) s_max = 0ull;
-    for (int e = threadIdx.x; e < d.nz; e += blockDim.x) {
+    cta_stage(z, v.z + static_cast<long>(p) * d.nz, d.nz, [&](int e) {
       const int t = e / (nx + nu);
-      z[t * P + (e - t * (nx + nu))] = v.z[static_cast<long>(p) * d.nz + e];
-    }
-    for (int e = threadIdx.x; e < d.nl; e += blockDim.x)
-      lam[(e / nx) * Q + e % nx] = v.lam[static_cast<long>(p) * d.nl + e];
-    for (int e = threadIdx.x; e < d.nth; e += blockDim.x) th[e] = v.theta[static_cast<long>(p) * d.nth + e];
+      return t * P + (e - t * (nx + nu));
+    });
+    cta_stage(lam, v.lam + static_cast<long>(p) * d.nl, d.nl, [&](int e) { return (e / nx) * Q + e % nx; });
+    cta_stage(th, v.theta + static_cast<long>(p) * d.nth, d.nth);
     __syncthreads();
     double m = 0.0;
     for (int t = threadIdx.x; t <= T; t += blockDim.x) {
@@ -393,8 +393,10 @@ __global__ void __launch_bounds__(128) vjp_kernel(View v, const int* __restrict_
       double* szt = sz_ + nz;
       double* sl = szt + nz;
       double* slt = sl + nl;
-      for (int e = threadIdx.x; e < nz; e += blockDim.x) sz_[e] = z[e], szt[e] = zt[e];
-      for (int e = threadIdx.x; e < nl; e += blockDim.x) sl[e] = lam[e], slt[e] = lt[e];
+      cta_stage<4>(sz_, z, nz);
+      cta_stage<4>(szt, zt, nz);
+      cta_stage<4>(sl, lam, nl);
+      cta_stage<4>(slt, lt, nl);
       z = sz_, zt = szt, lam = sl, lt = slt;
     }
     __syncthreads();
