@@ -705,10 +705,21 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
   // reads the count back only at iterations 4, 8, 16, ... to stop early
   // (one synchronisation for the benchmark's max_sqp_iters = 5).
   int n_bound = b->B;  // upper bound of the active count, sizes the grids
-  for (int iter = 0; iter < cfg->max_sqp_iters && n_bound > 0; ++iter) {
+  // The affine-quadratic family's Q_t, R_t (diagonal cost Hessians, then
+  // project_pd), A_t and B_t depend on theta only, never on z
+  // (affine_quadratic.hpp:39-81, quadratic_cost.hpp:9-20), so the -S / Phi^-1
+  // blocks assembled at the first iteration are, bit for bit, the ones every
+  // later re-linearisation of this solve would assemble (same theta, same
+  // eps_pd, same arithmetic). Later iterations and the final refresh re-run
+  // the linearisation (q_t, r_t, C_t, the evaluation checks) and keep the
+  // blocks; a Cholesky that fails on them failed at the first iteration.
+  const bool keep_blocks = b->prob.family == DOCP_AFFINE_QUADRATIC && !std::getenv("DOCP_REASSEMBLE");
+  int ran = 0;
+  for (int iter = 0; iter < cfg->max_sqp_iters && n_bound > 0; ++iter, ++ran) {
     const int* list = b->list[cur];
     const int* cnt = b->counts + 1 + cur;
-    if ((rc = launch_assemble(b, list, cnt, n_bound, cfg->eps_pd, 1, cfg->pcg.mode == DOCP_PCG_FAST))) return rc;
+    const int schur = iter == 0 || !keep_blocks;
+    if ((rc = launch_assemble(b, list, cnt, n_bound, cfg->eps_pd, schur, cfg->pcg.mode == DOCP_PCG_FAST))) return rc;
     if ((rc = launch_gamma(b, list, cnt, n_bound, DOCP_RHS_FORWARD))) return rc;
     if ((rc = launch_pcg(b, cfg->pcg, list, cnt, n_bound, b->v.lam))) return rc;
     if ((rc = launch_recover(b, list, cnt, n_bound, b->v.lam, DOCP_RHS_FORWARD))) return rc;
@@ -729,7 +740,10 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
   int* fin_cnt = b->counts + 1 + (cur ^ 1);
   ok_list_kernel<<<grid_for(b->B, 256, 4096), 256, 0, b->stream>>>(b->v, fin, fin_cnt);
   LAUNCH_CHECK();
-  if ((rc = launch_assemble(b, fin, fin_cnt, b->B, cfg->eps_pd, 1, cfg->pcg.mode == DOCP_PCG_FAST))) return rc;
+  // every problem of fin was in the first iteration's list (init_solve lists
+  // exactly the OK problems; statuses never return to OK)
+  const int schur = !(keep_blocks && ran > 0);
+  if ((rc = launch_assemble(b, fin, fin_cnt, b->B, cfg->eps_pd, schur, cfg->pcg.mode == DOCP_PCG_FAST))) return rc;
   if ((rc = launch_kkt(b, fin, fin_cnt, b->B))) return rc;
   return DOCP_OK;
 }

@@ -599,3 +599,48 @@ def test_fast_nx8_kernels_agree(D, nx, nu, T, monkeypatch):
     assert np.array_equal(got[""][1], got["h8r"][1])
     for j in range(5):
         assert rel(got[""][0][j], got["h8r"][0][j]) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_aq_blocks_kept_across_sqp_iterations(D, mode, monkeypatch):
+    """The affine-quadratic family's -S / Phi^-1 depend on theta only, so
+    docp_sqp_solve assembles them once per solve and later iterations (and
+    the final refresh, sqp.hpp:254-259) only re-linearise. The kept blocks
+    must equal a fresh assembly at the returned trajectory bit for bit, and
+    the whole solve + backward must equal a run that re-assembles every
+    iteration (DOCP_REASSEMBLE)."""
+    nx, nu, T, B = 8, 4, 30, 8
+    th = aq_thetas(nx, nu, T, 31, B)
+    prob = D.affine_quadratic(nx, nu, T)
+    nz, nl = D.sizes(prob)
+    z0 = np.random.default_rng(3).standard_normal((B, nz))
+    cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(mode=mode))
+    lg = np.random.default_rng(4).standard_normal((B, nz))
+
+    def run():
+        b = D.Batch(prob, B)
+        b.upload(D._lib.F_THETA, th)
+        b.upload(D._lib.F_Z, z0)
+        b.upload(D._lib.F_LAMBDA, np.zeros((B, nl)))
+        b.sqp_solve(cfg)
+        assert all(e is None for e in b.errors())
+        assert (b.download(D._lib.F_SQP_ITERS) >= 2).all()  # blocks were reused at least once
+        kept = b.download_schur()
+        b.upload(D._lib.F_LOSS_GRAD_Z, lg)
+        b.upload(D._lib.F_LAMBDA_TILDE, np.zeros((B, nl)))
+        b.backward_vjp(cfg.pcg)
+        out = [b.download(f) for f in (D._lib.F_Z, D._lib.F_LAMBDA, D._lib.F_GRAD_THETA, D._lib.F_LAMBDA_TILDE,
+                                       D._lib.F_KKT, D._lib.F_PCG_HISTORY, D._lib.F_STEP_SIZES)]
+        if mode == "parity":  # docp_assemble_schur is the reference's arithmetic
+            b.linearize()          # fresh assembly at the returned trajectory
+            b.assemble_schur()
+            fresh = b.download_schur()
+            for k, f in zip(kept, fresh):
+                assert np.array_equal(k, f)
+        return out + list(kept)
+
+    kept_run = run()
+    monkeypatch.setenv("DOCP_REASSEMBLE", "1")
+    full_run = run()
+    for a, c in zip(kept_run, full_run):
+        assert np.array_equal(a, c)
