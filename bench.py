@@ -67,9 +67,48 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.nvml = index, [], None, None
+
+    def _nvml_handle(self):
+        """NVML handle of this rank's device (by PCI bus id, so CUDA_VISIBLE_DEVICES cannot confuse it)."""
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self):
+        """NVML every 5 ms: a timed region of ~0.2 s gets tens of samples (nvidia-smi -lms 100 gets one)."""
+        p, h = self.nvml
+        bits = [("hw_slowdown", p.nvmlClocksEventReasonHwSlowdown),
+                ("hw_thermal_slowdown", p.nvmlClocksEventReasonHwThermalSlowdown),
+                ("sw_thermal_slowdown", p.nvmlClocksEventReasonSwThermalSlowdown),
+                ("sw_power_cap", p.nvmlClocksEventReasonSwPowerCap)]
+        smax = str(p.nvmlDeviceGetMaxClockInfo(h, p.NVML_CLOCK_SM))
+        while not self.stop:
+            try:
+                sm = p.nvmlDeviceGetClockInfo(h, p.NVML_CLOCK_SM)
+                pw = p.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = p.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((time.time(), [str(sm), smax, "%.2f" % pw]
+                                  + ["Active" if rs & b else "Not Active" for _, b in bits]))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __enter__(self):
+        try:
+            self.nvml = self._nvml_handle()
+            self.stop = False
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -87,6 +126,9 @@ class ClockSampler:
                 self.rows.append((time.time(), parts[1:]))
 
     def __exit__(self, *exc):
+        if self.nvml:
+            self.stop = True
+            self.thread.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
@@ -99,7 +141,7 @@ class ClockSampler:
 
     def summary(self):
         t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", time.time())
-        rows = [r for (ts, r) in self.rows if t0 <= ts <= t1 + 0.15]
+        rows = [r for (ts, r) in self.rows if t0 <= ts <= t1 + (0.01 if self.nvml else 0.15)]
         if not rows:  # timed region shorter than one sample period: nearest samples
             rows = [r for (ts, r) in sorted(self.rows, key=lambda x: abs(x[0] - t0))[:2]]
         self.rows = rows
@@ -110,7 +152,8 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
                 "power_w_max": max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()),
-                "samples": len(self.rows), "reasons": reasons}
+                "samples": len(self.rows), "sampler": "nvml 5 ms" if self.nvml else "nvidia-smi 100 ms",
+                "reasons": reasons}
 
 
 # --------------------------------------------------------------------------- reference arm (CPU)
