@@ -9,12 +9,17 @@ GPU: per instance a warm-started SQP solve (max 5 iterations, PCG eps 1e-12)
 from its expert demonstration, the control-matching loss, one adjoint PCG
 solve + theta-VJP, then the fixed-order gradient sum, its exchange across
 GPUs (NCCL all-gather, rank-order sum) and the gradient step on the shared
-state-cost weights. value = problems/s over all GPUs (weak scaling: 4096 per
-GPU), timed on the device with CUDA events, max over ranks.
+state-cost weights. value = problems/s over all GPUs, timed on the device
+with CUDA events, max over ranks. Weak scaling (default): 4096 problems per
+GPU; --scaling strong: 4096 in total, split in contiguous ranges
+(common.hpp:84-97 chunking).
 
     python bench.py [--gpus N --steps K --warmup W]        our CUDA path
     python bench.py --impl reference ...                   the reference CPU solver
                                                            (oracle/_ref) on the host cores
+
+--gpus N > 1 outside torchrun re-launches itself under torch.distributed.run
+with N ranks (127.0.0.1); under torchrun WORLD_SIZE must equal N.
 """
 from __future__ import annotations
 
@@ -43,8 +48,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=4096, help="problems per GPU")
+    ap.add_argument("--batch", type=int, default=4096,
+                    help="problems per GPU (weak scaling) or in total (strong scaling)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --batch problems per GPU; strong: --batch problems split over the GPUs")
     ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
+    ap.add_argument("--no-parity-pass", action="store_true",
+                    help="skip the PARITY-mode pass and the FAST/PARITY iteration-count tally")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU time of the baseline sample")
     return ap.parse_args()
@@ -189,6 +199,17 @@ def cpu_epochs(po, prob, th, demos, w0, epochs, kind):
     return times
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -211,7 +232,7 @@ def measure_cpu_baseline(target_s, kind="reference"):
     n = int(min(4096, max(cores, cores * round(target_s / 2 / max(t, 1e-3)))))
     po_, prob, th, demos = reference_sample(n) if kind == "reference" else _port_sample(po, n)
     times = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 2, lib_kind)
-    return {"value": n / times[1], "unit": "problems/s", "cores": cores, "kind": kind,
+    return {"value": n / times[1], "unit": "problems/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
             "sample": f"{n} of the 4096 C3 problems (random_convex_instance(8,4,100), seed 0), one warm IL epoch "
                       f"(second of two) through parallel_for with {cores} workers: {times[1]:.2f} s"}
 
@@ -238,14 +259,18 @@ def run_reference(args):
     if not po.available("ref"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference here)"}))
         return 0
-    # size one epoch to ~ a few seconds on this host
+    # The whole batch (the GPU arm's config) when its epochs fit ~4 minutes on
+    # this host, else a bounded sample: per-problem work is the same draw-for-
+    # draw (problem j is the j-th random_convex_instance either way).
     po_, prob, th, demos = reference_sample(cores)
     t1 = cpu_epochs(po_, prob, th, demos, np.full(NX, 0.5), 1, "ref")[0]
-    per_epoch_target = 150.0 / max(1, args.steps + args.warmup)
-    n = int(min(args.batch, max(cores, cores * round(per_epoch_target / 2 / max(t1, 1e-3)))))
+    per_problem = t1 / cores * 1.15  # + the expert solves
+    budget = 240.0
+    full = per_problem * args.batch * (args.steps + args.warmup) <= budget
+    n = args.batch if full else int(min(args.batch, max(cores, cores * round(
+        budget / (args.steps + args.warmup) / max(per_problem * cores, 1e-6)))))
     po_, prob, th, demos = reference_sample(n)
-    import paper_2510_06179_b200 as D  # host-side uniform draw only (train.hpp:61-64 recipe)
-    w0 = D.generate_uniform(0, NX)
+    w0 = po.gen_uniform(0, NX)  # train_il's learnable-weight draw (train.hpp:61-64), reference build
     times = cpu_epochs(po_, prob, th, demos, w0, args.warmup + args.steps, "ref")[args.warmup:]
     secs = float(np.sum(times))
     value = n * args.steps / secs
@@ -254,10 +279,14 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: the reference's random_convex_instance(8,4,100) draws (mt19937_64 seed 0) with "
                     "its own expert demonstrations",
-            "config": {"workload": "C3 imitation-learning epoch (train_il body) on a bounded sample",
-                       "batch_per_step": n, "horizon": T, "n_x": NX, "n_u": NU, "max_sqp_iters": 5,
-                       "pcg_epsilon": 1e-12},
+            "config": {"workload": "C3 imitation-learning epoch (train_il body)" +
+                                   ("" if full else " on a bounded sample"),
+                       "batch_per_step": n, "same_batch_as_gpu_arm": full, "horizon": T, "n_x": NX, "n_u": NU,
+                       "max_sqp_iters": 5, "pcg_epsilon": 1e-12,
+                       "per_problem_invariance": "problem j is the j-th sequential random_convex_instance(8,4,100) "
+                                                 "draw in both arms; a sample is the first n of the 4096"},
             "cpu_baseline": {"value": value, "unit": "problems/s", "cores": cores, "kind": "reference",
+                             "cpu_model": cpu_model(),
                              "sample": f"{n} problems per epoch, reference headers + eigen_lite, parallel_for "
                                        f"with {cores} workers"},
             "e2e": {"value": value, "unit": "problems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -274,7 +303,8 @@ def run_ours(args):
 
     import paper_2510_06179_b200 as D
     from paper_2510_06179_b200 import _lib as L
-    from paper_2510_06179_b200.distributed import fixed_order_allreduce
+    from paper_2510_06179_b200.distributed import fixed_order_allreduce, global_batch as job_batch, \
+        max_over_ranks, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -285,13 +315,18 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
 
-    B = args.batch
     prob = D.affine_quadratic(NX, NU, T)
     nz, nl = D.sizes(prob)
     nth = D.theta_size(prob)
-    # this rank's contiguous shard of one sequential draw (generators.hpp:102-111)
-    th_all = D.generate_affine_quadratic(NX, NU, 0, B * world)
-    thetas = th_all[rank * B:(rank + 1) * B].copy()
+    # this rank's contiguous shard of one sequential draw (generators.hpp:102-111):
+    # weak scaling draws batch x world problems, strong scaling splits batch
+    global_batch = job_batch(args.batch, world, args.scaling)
+    lo, hi = shard_range(global_batch, rank, world)
+    B = hi - lo
+    if B < 1:
+        raise SystemExit(f"rank {rank}: empty shard ({global_batch} problems over {world} ranks)")
+    th_all = D.generate_affine_quadratic(NX, NU, 0, global_batch)
+    thetas = th_all[lo:hi].copy()
 
     # expert demonstrations: sqp_solve at theta* (default SqpConfig), on the GPU, untimed
     expert = thetas.copy()
@@ -315,11 +350,11 @@ def run_ours(args):
     b.upload(L.F_LAMBDA_TILDE, np.zeros((B, nl)))
     out = torch.zeros(1 + NX, dtype=torch.float64, device=dev)  # [loss | grad]
     cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode=args.mode))
-    den = float(B * world)
+    den = float(global_batch)
 
-    def epoch(demo_buf=None):
+    def epoch(demo_buf=None, c=cfg):
         dptr = (demos if demo_buf is None else demo_buf).data_ptr()
-        b.il_epoch(cfg, w.data_ptr(), 0, NX, dptr, den, out.data_ptr(), out.data_ptr() + 8)
+        b.il_epoch(c, w.data_ptr(), 0, NX, dptr, den, out.data_ptr(), out.data_ptr() + 8)
         tot = fixed_order_allreduce(out) if world > 1 else out
         w.sub_(LR * tot[1:])
         return tot
@@ -369,13 +404,11 @@ def run_ours(args):
         barrier()
         clocks.mark(False)
     launches = D.kernel_launches() - launches0
+    b.il_check()  # train_il fails the epoch on any failed demonstration (train.hpp:111-119)
     ms = start.elapsed_time(stop)
     loss_last = float(tot[0].item())
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    value = B * world * args.steps / (ms_max / 1e3)
+    ms_max = max_over_ranks(ms, dev)
+    value = global_batch * args.steps / (ms_max / 1e3)
 
     # per-kernel profile of the same steps (CUDA events on the launching stream)
     restore(state0)
@@ -450,12 +483,49 @@ def run_ours(args):
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
-    et = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = B * world * args.steps / (float(et.item()) / 1e3)
+    e2e_value = global_batch * args.steps / (max_over_ranks(e2e_ms, dev) / 1e3)
     h2d = thetas.nbytes + demos_host.nbytes
     d2h = 8 * (1 + NX)
+
+    # PARITY pass (bitwise the reference's arithmetic, test_gpu_parity.py) over
+    # the same post-warm-up epochs, and the per-instance iteration-count tally
+    # of the benched mode against it on the first of them (identical inputs)
+    parity = None
+    if args.mode == "fast" and not args.no_parity_pass:
+        pcfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode="parity"))
+
+        def counts():
+            return (b.download(L.F_SQP_ITERS).ravel().copy(), b.download(L.F_PCG_HISTORY).copy(),
+                    b.download(L.F_PCG_ITERS).ravel().copy())
+        restore(state0)
+        epoch()
+        cf = counts()
+        restore(state0)
+        epoch(c=pcfg)
+        cp = counts()
+        fwd_diff = int(sum(np.sum(cf[1][j, :cp[0][j]] != cp[1][j, :cp[0][j]]) for j in range(B)))
+        tally = {"instances": B, "sqp_count_mismatches": int(np.sum(cf[0] != cp[0])),
+                 "forward_pcg_solves": int(np.sum(cp[0])), "forward_pcg_count_mismatches": fwd_diff,
+                 "backward_pcg_count_mismatches": int(np.sum(cf[2] != cp[2])),
+                 "max_abs_count_difference": int(max(np.abs(cf[2] - cp[2]).max(), max(
+                     (np.abs(cf[1][j, :cp[0][j]] - cp[1][j, :cp[0][j]]).max() for j in range(B) if cp[0][j]),
+                     default=0)))}
+        restore(state0)
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(args.steps):
+            epoch(c=pcfg)
+        q1.record(stream)
+        barrier()
+        b.il_check()
+        pms = max_over_ranks(q0.elapsed_time(q1), dev)
+        pv = global_batch * args.steps / (pms / 1e3)
+        parity = {"value": pv, "unit": "problems/s", "ms_per_step": pms / args.steps,
+                  "frac_of_benched_mode": pv / value,
+                  "note": "PARITY mode: no FMA contraction, reference fold orders (btd_matvec diag->sub->super, "
+                          "block_dot in block-index order); bit-identical to the reference build",
+                  "count_tally_vs_parity": tally}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -468,13 +538,14 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: random_convex_instance(8,4,100) draws (reference recipe, mt19937_64 seed 0), "
                     "expert demonstrations solved on the GPU at w*",
             "config": {"workload": "C3 imitation-learning epoch (train_il body): solve + adjoint gradient + "
                                    "fixed-order sum + theta-gradient exchange + GD step",
-                       "batch_per_gpu": B, "global_batch": B * world, "horizon": T, "n_x": NX, "n_u": NU,
+                       "batch_per_gpu": B, "global_batch": global_batch, "horizon": T, "n_x": NX, "n_u": NU,
                        "max_sqp_iters": 5, "pcg_epsilon": 1e-12, "pcg_mode": args.mode,
                        "parallelism": f"dp{world} (instance sharding)",
                        "l2": "inputs larger than L2: %.0f MB of Schur blocks per GPU" %
@@ -490,6 +561,7 @@ def run_ours(args):
                                  "latency-bound (two reductions, four barriers)",
                          "smem_peak_derived": smem_peak, "frac_smem": achieved / smem_peak},
             "cpu_baseline": cpu,
+            "parity_mode": parity,
             "e2e": {"value": e2e_value, "unit": "problems/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "loss_last": host_results[-1][0], "same_epochs_as_timed": host_results[-1][0] == loss_last},
             "clocks": clocks.summary(),
@@ -510,8 +582,29 @@ def run_ours(args):
     return 0
 
 
+def spawn_command(args, argv):
+    """`--gpus N` outside torchrun: the same command under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1), as the driver launches it."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
 def main():
     args = parse()
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        return subprocess.call(spawn_command(args, sys.argv[1:]))
+    if world is not None and int(world) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        return 2
+    if args.gpus > 1:
+        # communicator set-up lines (ranks, NVLS / P2P transports) in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -30,14 +30,16 @@ def _stale(target, sources):
 UNITS = ["docp_cuda.cu", "pcg_nx8.cu", "pcg_nx4.cu", "pcg_nx16.cu", "pcg_nxrt.cu", "generators.cpp"]
 
 
-def build_cuda(force=False, verbose=False):
-    """Compiles the translation units in parallel, then links the shared library."""
+def build_cuda(force=False, verbose=False, lib=None, extra_flags=()):
+    """Compiles the translation units in parallel, then links the shared library.
+    lib / extra_flags: an A/B variant (e.g. -DDOCP_H8P_CLOCK) built elsewhere."""
+    LIB_ = lib or LIB
     sources = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "docp_cuda.h")]
-    if not force and not _stale(LIB, sources):
+    if not force and not _stale(LIB_, sources):
         return
-    objdir = os.path.join(os.path.dirname(LIB), "obj")
+    objdir = os.path.join(os.path.dirname(LIB_), "obj")
     os.makedirs(objdir, exist_ok=True)
-    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra_flags)
     procs = []
     for unit in UNITS:
         obj = os.path.join(objdir, unit + ".o")
@@ -49,7 +51,7 @@ def build_cuda(force=False, verbose=False):
         if p.wait() != 0:
             failed.append(unit)
         log.close()
-    with open(os.path.join(os.path.dirname(LIB), "ptxas.log"), "w") as out:
+    with open(os.path.join(os.path.dirname(LIB_), "ptxas.log"), "w") as out:
         for unit in UNITS:
             out.write(open(os.path.join(objdir, unit + ".log")).read())
     if failed:
@@ -57,11 +59,11 @@ def build_cuda(force=False, verbose=False):
             sys.stderr.write(open(os.path.join(objdir, unit + ".log")).read())
         raise RuntimeError(f"nvcc failed: {failed}")
     objs = [os.path.join(objdir, u + ".o") for u in UNITS]
-    r = subprocess.run(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs])
+    r = subprocess.run(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB_, *objs])
     if r.returncode != 0:
         raise RuntimeError("link failed")
     if verbose:
-        print("built", LIB)
+        print("built", LIB_)
 
 
 CLI_SRC = os.path.join(ROOT, "paper_2510_06179_b200", "cli")

@@ -204,7 +204,12 @@ int docp_line_search(docp_batch* batch, const docp_sqp_config* cfg);
 int docp_kkt_residual(docp_batch* batch); /* KKT <- ||F(Z, LAMBDA)||_inf */
 /* Full forward pass; Z and LAMBDA hold the initial guess and receive the
  * solution; the final QpData/Schur system stay resident for backward.
- * Synchronizes once per SQP iteration. */
+ * The loop is enqueued without waiting on the device: every kernel reads the
+ * active-problem count from device memory, and the host reads it back only
+ * after SQP iterations 4, 8, 16, ... to stop early (one synchronization for
+ * max_sqp_iters = 5). For the affine-quadratic family the -S / Phi^-1 blocks
+ * depend on theta only, so they are assembled at the first iteration and kept
+ * (bitwise the reference's re-assembly; DOCP_REASSEMBLE=1 forces it). */
 int docp_sqp_solve(docp_batch* batch, const docp_sqp_config* cfg);
 /* backward_vjp on the resident forward result: LOSS_GRAD_Z and the warm
  * LAMBDA_TILDE in; GRAD_THETA, LAMBDA_TILDE, PCG_ITERS out. */
@@ -221,6 +226,14 @@ int docp_backward_vjp(docp_batch* batch, const docp_pcg_config* cfg);
 int docp_il_epoch(docp_batch* batch, const docp_sqp_config* cfg, const double* weights, int32_t learn_start,
                   int32_t learn_size, const double* demos, double loss_denominator, double* loss_sum,
                   double* grad_sum);
+/* The reference fails an epoch on the first demonstration whose solve or
+ * backward threw (train.hpp:111-119). docp_il_epoch never synchronizes, so
+ * instead a failed demonstration contributes zero to both sums, and is
+ * counted on the device. This call waits for the batch's stream, returns the
+ * number of failed demonstrations in the epochs since the last call and the
+ * smallest failed index (-1 if none), and resets both. STATUS holds the
+ * failures of the last epoch (docp_format_status renders them). */
+int docp_il_failures(docp_batch* batch, int32_t* n_failed, int32_t* first_failed);
 
 /* Closed-loop MPC rollouts (batch.hpp:172-212) with the benchmark tasks'
  * environments: affine-quadratic instances step their own dynamics with

@@ -160,6 +160,8 @@ def load(kind: str):
             lib.ref_train_il_cartpole.restype = C.c_int
             lib.ref_train_il_cartpole.argtypes = [C.c_uint64, C.c_int, C.c_int, dp, C.c_int, C.c_double, dp,
                                                   C.POINTER(C.c_long), C.POINTER(C.c_long), dp, sp]
+            lib.ref_gen_uniform.restype = None
+            lib.ref_gen_uniform.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, dp]
             lib.ref_spectral_radius.restype = C.c_double
             lib.ref_spectral_radius.argtypes = [dp, C.c_int]
             lib.ref_pcg_invocations.restype = C.c_ulonglong
@@ -350,6 +352,13 @@ def il_epoch(kind, prob, thetas, demos, lam_cache, lt_cache, cfg, learn_start, l
     if rc:
         raise OracleError(st)
     return loss.value, grad, losses, grads, sqp_it, pcg_it
+
+
+def gen_uniform(seed, n, lo=0.0, hi=1.0):
+    """Reference recipe of train_il's learnable-weight draw (train.hpp:61-64; ref only)."""
+    out = np.zeros(n)
+    load("ref").ref_gen_uniform(seed, n, lo, hi, _p(out))
+    return out
 
 
 def gen_aq(nx, nu, T, seed, count, convex=True):

@@ -570,6 +570,14 @@ void ref_gen_aq(int nx, int nu, int horizon, std::uint64_t seed, int count, int 
   }
 }
 
+/// The learnable-weight draw of train_il (train.hpp:61-64): n values of
+/// uniform_real_distribution(lo, hi) from mt19937_64(seed), in order.
+void ref_gen_uniform(std::uint64_t seed, int n, double lo, double hi, double* out) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unit(lo, hi);
+  for (int i = 0; i < n; ++i) out[i] = unit(rng);
+}
+
 /// Reference spectral radius (generators.hpp:41-46) of an n x n col-major matrix.
 double ref_spectral_radius(const double* a, int n) {
   return bench::spectral_radius(Matrix(Eigen::Map<const Matrix>(a, n, n)));

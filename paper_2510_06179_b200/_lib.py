@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdocp_cuda.so")
+LIB_PATH = os.environ.get("DOCP_LIB_PATH") or os.path.join(HERE, "lib", "libdocp_cuda.so")  # override: A/B builds
 
 AFFINE_QUADRATIC, CARTPOLE, ATTITUDE = 1, 2, 3
 OK, DIMENSION, EVALUATION, NUMERICAL, BREAKDOWN, DIVERGENCE, UNSUPPORTED, CUDA_ERROR, INVALID = range(9)
@@ -84,6 +84,7 @@ SIGNATURES = {
     "docp_sqp_solve": (C.c_int, [_vp, C.POINTER(SqpConfigC)]),
     "docp_backward_vjp": (C.c_int, [_vp, C.POINTER(PcgConfigC)]),
     "docp_il_epoch": (C.c_int, [_vp, C.POINTER(SqpConfigC), _vp, _i32, _i32, _vp, _dbl, _vp, _vp]),
+    "docp_il_failures": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
     "docp_rollout": (C.c_int, [_vp, C.POINTER(SqpConfigC), _vp, _i32, _i32]),
     "docp_rollout_backward": (C.c_int, [_vp, C.POINTER(PcgConfigC)]),
     "docp_generate_affine_quadratic": (C.c_int, [_i32, _i32, _u64, _i32, _i32, _dp]),

@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -386,6 +386,25 @@ class Batch:
         c = cfg.c()
         _raise_call(L.lib().docp_il_epoch(self.h, C.byref(c), weights_ptr, learn_start, learn_size, demos_ptr,
                                           loss_denominator, loss_sum_ptr, grad_sum_ptr))
+
+    def il_failures(self) -> Tuple[int, int]:
+        """(failed demonstrations since the last call, first failed index or -1);
+        waits for the batch's stream and resets the count."""
+        n, first = C.c_int32(0), C.c_int32(0)
+        _raise_call(L.lib().docp_il_failures(self.h, C.byref(n), C.byref(first)))
+        return int(n.value), int(first.value)
+
+    def il_check(self, epoch: int = 0):
+        """Raises like train_il (train.hpp:111-119) when a demonstration of the
+        epochs since the last check failed: "epoch E, demonstration J: <error>"."""
+        n, first = self.il_failures()
+        if n:
+            st = self.download(L.F_STATUS)[first]
+            err = status_error(L.Status(*[int(x) for x in st]))
+            msg = f"epoch {epoch}, demonstration {first}: {err}"
+            if isinstance(err, BreakdownError):
+                raise BreakdownError(msg, err.iteration)
+            raise type(err)(msg)
 
 
     def rollout(self, cfg: SqpConfig, x_init, episode_length: int):

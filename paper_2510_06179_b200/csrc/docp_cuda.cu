@@ -125,7 +125,11 @@ __global__ void ok_list_kernel(View v, int* __restrict__ out, int* __restrict__ 
 
 __global__ void iota_kernel(int* out, int n, int* count) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) out[k] = k;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count = n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    count[0] = n;
+    count[4] = 0;           // IL epochs: failed demonstrations since the last docp_il_failures
+    count[5] = 0x7fffffff;  // ... and the first of them
+  }
 }
 
 __global__ void reset_status_kernel(View v) {
@@ -912,7 +916,8 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
   LAUNCH_CHECK();
   if ((rc = docp_backward_vjp(b, &cfg->pcg))) return rc;
   if (cfg->pcg.mode == DOCP_PCG_FAST) {
-    il_sum_tree_kernel<<<1 + learn_size, kIlTreeThreads, 0, b->stream>>>(b->v, learn_start, loss_sum, grad_sum);
+    il_sum_tree_kernel<<<1 + learn_size, kIlTreeThreads, 0, b->stream>>>(b->v, learn_start, loss_sum, grad_sum,
+                                                                        b->counts + 4);
   } else {
     const int cols = 1 + learn_size;
     const int ctas = (cols + kIlSumThreads - 1) / kIlSumThreads;
@@ -921,9 +926,23 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
     const int rows = std::max(1, std::min(b->B, (160 * 1024 / 8) / ncol - 1));
     const size_t smem = static_cast<size_t>(rows | 1) * ncol * sizeof(double);
     CUDA_TRY(cudaFuncSetAttribute(il_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    il_sum_kernel<<<ctas, kIlSumThreads, smem, b->stream>>>(b->v, learn_start, learn_size, rows, loss_sum, grad_sum);
+    il_sum_kernel<<<ctas, kIlSumThreads, smem, b->stream>>>(b->v, learn_start, learn_size, rows, loss_sum, grad_sum,
+                                                            b->counts + 4);
   }
   LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+int docp_il_failures(docp_batch* b, int32_t* n_failed, int32_t* first_failed) {
+  if (!b || !n_failed || !first_failed) return fail(DOCP_INVALID, "null argument");
+  int h[2];
+  CUDA_TRY(cudaMemcpyAsync(h, b->counts + 4, sizeof h, cudaMemcpyDeviceToHost, b->stream));
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  *n_failed = h[0];
+  *first_failed = h[0] ? h[1] : -1;
+  const int reset[2] = {0, 0x7fffffff};
+  CUDA_TRY(cudaMemcpyAsync(b->counts + 4, reset, sizeof reset, cudaMemcpyHostToDevice, b->stream));
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
   return DOCP_OK;
 }
 
@@ -1041,8 +1060,11 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   else if (cl > 1) snprintf(fast, sizeof fast, "%s(cluster%d,resident)", fk, cl);
   else snprintf(fast, sizeof fast, "%s", d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
                                                    : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>");
-  const char* parity = d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
-                                  : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>";
+  const int p8 = d.nx == 8 ? h8p_variant_for(d, dev) : 0;
+  const char* parity = p8 == 1   ? "pcg_kernel_h8p<prefetch>; uploaded systems pcg_kernel_h8"
+                       : p8 == 2 ? "pcg_kernel_h8p<no-prefetch>; uploaded systems pcg_kernel_h8"
+                       : d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
+                                   : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>";
   return snprintf(buf, cap, "nx=%d layout=%s record=%ld B parity=%s(%s) fast=%s", d.nx,
                   d.nx == 8 ? "swizzle8" : d.nx == 4 ? "swizzle4" : "colmajor", d.blk_stride * 8, parity,
                   res ? "resident" : "streaming", fast);

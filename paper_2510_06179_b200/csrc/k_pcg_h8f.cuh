@@ -59,10 +59,15 @@ __device__ __forceinline__ void load_rows(const double* blk, const Bases& bs, do
 __host__ __device__ inline int h8f_rows(const Dims& d, int cl) { return (d.nb + cl - 1) / cl; }
 
 /// Dynamic shared memory of pcg_kernel_h8f<*, CL> (doubles): four regions of
-/// R blocks, vbuf / xbuf with two halo rows, 3 x CL x 8 dot partials.
-__host__ __device__ inline long h8f_smem_doubles(const Dims& d, int cl) {
+/// R blocks, vbuf / xbuf with two halo rows (a second pair for CL > 1, whose
+/// (-S) product follows the Phi^-1 product with no barrier between), and
+/// 3 x CL x 8 dot partials. Where the second pair does not fit (dbuf =
+/// false: the longest horizons of a cluster size) the kernel puts a cluster
+/// barrier between the two products instead; it tells from its dynamic shared
+/// memory size which layout it was launched with.
+__host__ __device__ inline long h8f_smem_doubles(const Dims& d, int cl, bool dbuf = true) {
   const long R = h8f_rows(d, cl);
-  return 4 * R * 64 + 2 * (R + 2) * 8 + 3L * cl * 8;
+  return 4 * R * 64 + (cl > 1 && dbuf ? 4 : 2) * (R + 2) * 8 + 3L * cl * 8;
 }
 
 template <int CL>
@@ -100,7 +105,15 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
   double* sPu = sPd + R * 64;      // [R]
   double* vbuf = sPu + R * 64;     // [R + 2] x_i halves; slot = local row + 1, slots 0 / R+1 are halos
   double* xbuf = vbuf + (R + 2) * 8;  // [R + 2] hand-overs
-  double* red = xbuf + (R + 2) * 8;   // [3][CL][8] dot partials
+  // second pair for matvec_s_dot (CL > 1): it runs right after the Phi^-1
+  // product, whose phase-2 reads of the neighbours' slots (and of the halos
+  // the neighbour CTAs wrote) must not race with this product's phase-1 writes
+  uint32_t dyn_bytes;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
+  const bool dbuf = CL > 1 && dyn_bytes >= h8f_smem_doubles(d, CL, true) * 8;
+  double* vbuf2 = dbuf ? xbuf + (R + 2) * 8 : vbuf;
+  double* xbuf2 = dbuf ? vbuf2 + (R + 2) * 8 : xbuf;
+  double* red = dbuf ? xbuf2 + (R + 2) * 8 : xbuf + (R + 2) * 8;  // [3][CL][8] dot partials
 
   const int p = i & 1, m = (i >> 1) & 1;
   h8f::Bases bs;
@@ -341,10 +354,11 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8f(View v, const int* __r
       h8f::load_rows(SdI, bs, dd);
       h8f::load_rows(SsI, bs, oo);
       double own[4], low[4], up[4];
-      phase1(false, dd, oo, xr, vbuf, xbuf, own);
+      if (!dbuf) h8f_sync<CL>();  // the Phi^-1 product's phase-2 reads of vbuf / xbuf are done
+      phase1(false, dd, oo, xr, vbuf2, xbuf2, own);
       partial(a, b, slot);
       h8f_sync<CL>();
-      phase2(false, oo, vbuf, xbuf, low, up);
+      phase2(false, oo, vbuf2, xbuf2, low, up);
       finish(own, low, up, out);
     };
 

@@ -142,6 +142,11 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   const int my0 = voff(sv, 2 * h), my1 = voff(sv, 2 * h + 1);
   const int nx0 = voff(sv + 1, 2 * h), nx1 = voff(sv + 1, 2 * h + 1);
   const int pv0 = voff(sv - 1, 2 * h), pv1 = voff(sv - 1, 2 * h + 1);
+  // the (-S) product's hand-over goes one slot lower than the Phi^-1 one (row
+  // i writes slot i, reads slot i - 1): matvec_s_dot follows matvec_p with no
+  // barrier between, and this way the only slot it overwrites is the one this
+  // same thread has just read (row 0 reads slot 0, masked by has_prev)
+  const int pp0 = voff(max(sv - 2, 0), 2 * h), pp1 = voff(max(sv - 2, 0), 2 * h + 1);
   const int nf0 = voff(sv + 1, 0), nf1 = voff(sv + 1, 1), nf2 = voff(sv + 1, 2), nf3 = voff(sv + 1, 3);
   const uint32_t bd = static_cast<uint32_t>(nb) * 512u, bo = static_cast<uint32_t>(nb - 1) * 512u;
 
@@ -329,12 +334,12 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       put(vbuf, my0, my1, xr);
       h8s::sym_times(sd, xf, xr, h, own);
       rows_times(so, xf, hand);  // L_i x_i
-      put(xbuf, my0, my1, hand);
+      put(xbuf, pv0, pv1, hand);  // slot i (see pp0 above)
       partial(a, b, slot);
       __syncthreads();
       get(vbuf, nx0, nx1, xn);
       trans_times(so, xn, up);   // L_i' x_{i+1}
-      get(xbuf, pv0, pv1, low);
+      get(xbuf, pp0, pp1, low);
       finish(own, low, up, out);
     };
     // out = Phi^-1 x from shared memory. Two exchanges (x_{i+1}, then the

@@ -508,9 +508,22 @@ __global__ void __launch_bounds__(kIlLossThreads) il_loss_kernel(View v, const d
 /// in shared memory (coalesced, all loads in flight), then thread k folds its
 /// column in instance order.
 constexpr int kIlSumThreads = 256;
+/// A demonstration whose solve or backward failed contributes nothing (its
+/// loss and gradient rows are stale); column 0's pass counts it into
+/// fails[0] and the smallest such index into fails[1] (docp_il_failures), so
+/// the host can fail the epoch as train.hpp:111-119 does.
+__device__ __forceinline__ bool il_row_ok(const View& v, long p, int col, int* fails) {
+  if (v.status[p].code == DOCP_OK) return true;
+  if (col == 0) {
+    atomicAdd(fails, 1);
+    atomicMin(fails + 1, static_cast<int>(p));
+  }
+  return false;
+}
+
 __global__ void __launch_bounds__(kIlSumThreads) il_sum_kernel(View v, int learn_start, int learn_size, int rows,
                                                                double* __restrict__ loss_sum,
-                                                               double* __restrict__ grad_sum) {
+                                                               double* __restrict__ grad_sum, int* fails) {
   extern __shared__ double stage_buf[];  // [ncol][ld]: column-major, odd leading dimension
   const int c0 = blockIdx.x * kIlSumThreads;
   const int ncol = min(kIlSumThreads, 1 + learn_size - c0);
@@ -523,7 +536,9 @@ __global__ void __launch_bounds__(kIlSumThreads) il_sum_kernel(View v, int learn
     for (int g = threadIdx.x; g < n * ncol; g += blockDim.x) {
       const int j = g / ncol, c = g - j * ncol;
       const long p = p0 + j;
-      stage_buf[c * ld + j] = c0 + c == 0 ? v.loss[p] : v.grad[p * v.d.nth + learn_start + c0 + c - 1];
+      stage_buf[c * ld + j] = !il_row_ok(v, p, c0 + c, fails) ? 0.0
+                              : c0 + c == 0                 ? v.loss[p]
+                                                            : v.grad[p * v.d.nth + learn_start + c0 + c - 1];
     }
     __syncthreads();
     if (k < ncol) {
@@ -545,12 +560,14 @@ __global__ void __launch_bounds__(kIlSumThreads) il_sum_kernel(View v, int learn
 constexpr int kIlTreeThreads = 1024;
 __global__ void __launch_bounds__(kIlTreeThreads) il_sum_tree_kernel(View v, int learn_start,
                                                                      double* __restrict__ loss_sum,
-                                                                     double* __restrict__ grad_sum) {
+                                                                     double* __restrict__ grad_sum, int* fails) {
   __shared__ double part[kIlTreeThreads / 32];
   const int c = blockIdx.x;  // 0: loss, 1 + k: learnable gradient k
   double acc = 0.0;
   for (int p = threadIdx.x; p < v.B; p += blockDim.x)
-    acc += c == 0 ? v.loss[p] : v.grad[static_cast<long>(p) * v.d.nth + learn_start + c - 1];
+    acc += !il_row_ok(v, p, c, fails) ? 0.0
+           : c == 0                      ? v.loss[p]
+                                         : v.grad[static_cast<long>(p) * v.d.nth + learn_start + c - 1];
   acc = warp_sum(acc);
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
   __syncthreads();

@@ -4,6 +4,7 @@
 
 #include "k_pcg_h8.cuh"
 #include "k_pcg_h8f.cuh"
+#include "k_pcg_h8p.cuh"
 #include "k_pcg_h8r.cuh"
 #include "k_pcg_h8s.cuh"
 #include "pcg_launch.cuh"
@@ -35,7 +36,10 @@ template <int CL>
 int launch_h8f_cl(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
                   int max_iters) {
   auto kern = pcg_kernel_h8f<256, CL>;
-  const size_t smem = h8f_smem_doubles(b->d, CL) * sizeof(double);
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device);
+  size_t smem = h8f_smem_doubles(b->d, CL, true) * sizeof(double);
+  if (smem + 64 > static_cast<size_t>(max_optin)) smem = h8f_smem_doubles(b->d, CL, false) * sizeof(double);
   const int threads = (2 * h8f_rows(b->d, CL) + 31) / 32 * 32;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   cudaLaunchConfig_t lc{};
@@ -111,6 +115,44 @@ static int launch_h8s(docp_batch* b, const int* list, const int* count, int n_hi
   return DOCP_OK;
 }
 
+/// PARITY, one CTA per problem, device-assembled (symmetric) diagonal
+/// blocks: pcg_kernel_h8p (the reference's arithmetic with h8s's residency).
+/// Returns -1 (nothing launched) when the variant does not fit this shape.
+template <bool PREFETCH>
+static int launch_h8p(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
+                      int max_iters) {
+  auto kern = pcg_kernel_h8p<256, PREFETCH>;
+  const int threads = (2 * b->d.nb + 31) / 32 * 32;
+  if (threads > 256) return -1;
+  const size_t smem = h8p_smem_doubles<PREFETCH>(b->d) * sizeof(double);
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device);
+  if (smem + 256 > static_cast<size_t>(max_optin)) return -1;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) return -1;
+  const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
+  CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
+  ProfScope ps(b, DOCP_PROF_PCG);
+  kern<<<grid, threads, smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+/// The h8p variant for this shape (0: none): 1 = prefetching (T <= 112),
+/// 2 = no prefetch (T <= 127).
+int h8p_variant_for(const Dims& d, int device) {
+  if (d.nx != 8) return 0;
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  const int threads = (2 * d.nb + 31) / 32 * 32;
+  if (threads > 256) return 0;
+  if (h8p_smem_doubles<true>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 1;
+  if (h8p_smem_doubles<false>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 2;
+  return 0;
+}
+
 /// The h8s variant for this shape (0: none): 1 = prefetching, 256 threads
 /// (T <= 113); 2 = no prefetch, 256 threads (T <= 127); 3 = no prefetch, up
 /// to 384 threads at 168 registers (T <= 191).
@@ -136,7 +178,7 @@ int h8f_cluster_for(const Dims& d, int device) {
   for (int cl : {1, 2, 4, 8}) {
     if (cl > 1 && (cl - 1) * h8f_rows(d, cl) >= d.nb) break;  // every CTA must own a row
     if (cl < min_cl) continue;
-    if (h8f_rows(d, cl) <= 128 && h8f_smem_doubles(d, cl) * 8 + 64 <= static_cast<long>(max_optin)) return cl;
+    if (h8f_rows(d, cl) <= 128 && h8f_smem_doubles(d, cl, false) * 8 + 64 <= static_cast<long>(max_optin)) return cl;
   }
   return 0;
 }
@@ -154,6 +196,14 @@ static bool force_h8() { return force_variant("h8"); }
 /// blocks on-chip; PARITY (or no fitting cluster): two threads per block row
 /// (pcg_kernel_h8) up to T = 255, one thread per block row (pcg_kernel) beyond.
 DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
+  if (par && b->sym_blocks && !force_h8()) {
+    int rc = -1;
+    int var = h8p_variant_for(b->d, b->device);
+    if (var == 1 && force_variant("h8p_np")) var = 2;  // A/B: the no-prefetch form on a short horizon
+    if (var == 1) rc = launch_h8p<true>(b, list, count, n_hint, sol, eps, max_iters);
+    else if (var == 2) rc = launch_h8p<false>(b, list, count, n_hint, sol, eps, max_iters);
+    if (rc != -1) return rc;
+  }
   if (!par && !force_h8() && b->sym_blocks && !force_variant("h8r") && !force_variant("h8f")) {
     int rc = -1;
     int var = h8s_variant_for(b->d, b->device);
@@ -187,3 +237,12 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
 }
 
 }  // namespace docp_host
+
+#ifdef DOCP_H8P_CLOCK
+/// A/B builds only: cycles of pcg_kernel_h8p's thread 0 per phase, summed over launches (then reset).
+extern "C" int docp_h8p_clock(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, docp_dev::g_h8p_clk, 12 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  static const unsigned long long zero[16] = {0};
+  return cudaMemcpyToSymbol(docp_dev::g_h8p_clk, zero, sizeof zero) != cudaSuccess;
+}
+#endif

@@ -22,6 +22,24 @@ def shard_range(n: int, rank: int, world: int):
     return lo, min(n, lo + chunk)
 
 
+def global_batch(batch: int, world: int, scaling: str) -> int:
+    """Problems in the whole job: `batch` per rank (weak scaling) or `batch`
+    split over the ranks (strong scaling)."""
+    if scaling not in ("weak", "strong"):
+        raise ValueError(f"scaling must be weak or strong, not {scaling!r}")
+    return batch * world if scaling == "weak" else batch
+
+
+def max_over_ranks(x: float, device=None, group=None) -> float:
+    """The largest `x` over all ranks (a step time: the job ends with its
+    slowest rank)."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
 def fixed_order_allreduce(partial: torch.Tensor, group=None) -> torch.Tensor:
     """Sum of every rank's `partial`, added in rank order on every rank
     (0.0 + p_0 + p_1 + ...): deterministic and identical across ranks."""

@@ -98,3 +98,61 @@ def test_two_rank_gloo_epochs_match_single_process():
         w = w - 1e-2 * tot[1:]
     assert np.array_equal(w, res[0][1])
     assert np.allclose(w, g["final_weights"], rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------ bench.py rank logic (gloo, world size 2)
+
+
+def _bench_rank_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2510_06179_b200.distributed import global_batch, max_over_ranks
+    out = {}
+    for scaling in ("weak", "strong"):
+        gb = global_batch(4096, world, scaling)
+        out[scaling] = (gb, shard_range(gb, rank, world))
+    # each rank's step time differs; every rank must see the slowest
+    out["max"] = max_over_ranks(10.0 + rank)
+    # the exchanged [loss | grad] partials, summed in rank order on every rank
+    part = torch.tensor([0.1 * (rank + 1)] + [float(rank)] * 8, dtype=torch.float64)
+    out["sum"] = fixed_order_allreduce(part).numpy()
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+def test_bench_rank_logic_two_ranks():
+    """bench.py's per-rank shard (weak: 4096 per rank; strong: 4096 split),
+    the max-over-ranks step time and the rank-order gradient sum."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert res[0]["weak"] == (8192, (0, 4096)) and res[1]["weak"] == (8192, (4096, 8192))
+    assert res[0]["strong"] == (4096, (0, 2048)) and res[1]["strong"] == (4096, (2048, 4096))
+    assert res[0]["max"] == res[1]["max"] == 11.0
+    expect = (0.0 + np.array([0.1] + [0.0] * 8)) + np.array([0.2] + [1.0] * 8)
+    assert np.array_equal(res[0]["sum"], expect) and np.array_equal(res[1]["sum"], expect)
+
+
+def test_bench_gpus_flag_spawns_or_refuses():
+    """`bench.py --gpus N` outside torchrun re-launches itself with N ranks on
+    127.0.0.1; under torchrun a WORLD_SIZE that disagrees with --gpus is an error."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    cmd = bench.spawn_command(type("A", (), {"gpus": 4})(), ["--gpus", "4", "--steps", "2"])
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"] and cmd[-5].endswith("bench.py")
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2"], env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "WORLD_SIZE=3" in r.stderr

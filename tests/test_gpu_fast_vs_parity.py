@@ -46,3 +46,34 @@ def test_fast_matches_parity_on_c3_batch():
     assert len(diffs) <= 10
     assert rel_rows(zf, zp).max() <= 1e-9
     assert rel_rows(gf, gp).max() <= 1e-9
+
+
+def test_parity_kernels_agree_bitwise_on_c3_batch(monkeypatch):
+    """pcg_kernel_h8p (PARITY with registers + TMA residency, the benched
+    PARITY kernel) against pcg_kernel_h8 (PARITY, the plain form that
+    test_gpu_parity.py pins to the reference bit for bit on oracle-sized
+    cases): the whole 4096-problem C3 batch, forward and backward, every
+    field bit for bit and equal iteration counts."""
+    import paper_2510_06179_b200 as D
+    nx, nu, T, B = 8, 4, 100, 4096
+    prob = D.affine_quadratic(nx, nu, T)
+    nz, nl = D.sizes(prob)
+    th = D.generate_affine_quadratic(nx, nu, 0, B)
+    rng = np.random.default_rng(1)
+    z0 = 0.1 * rng.standard_normal((B, nz))
+    lg = rng.standard_normal((B, nz))
+    out = {}
+    for variant in ("h8p", "h8"):
+        if variant == "h8":
+            monkeypatch.setenv("DOCP_PCG_VARIANT", "h8")
+        cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(mode="parity"))
+        res, errs = D.sqp_solve_batch(prob, th, z0, np.zeros((B, nl)), cfg)
+        assert all(e is None for e in errs)
+        g, lt, its, errs = D.backward_vjp_batch(res[0].batch, lg, np.zeros((B, nl)), cfg.pcg)
+        assert all(e is None for e in errs)
+        out[variant] = (np.stack([r.z for r in res]), np.stack([r.lam for r in res]), [r.pcg_iters for r in res],
+                        [r.sqp_iters for r in res], g.copy(), lt.copy(), np.asarray(its).copy())
+    a, b = out["h8p"], out["h8"]
+    assert a[2] == b[2] and a[3] == b[3] and np.array_equal(a[6], b[6])
+    for k in (0, 1, 4, 5):
+        assert np.array_equal(a[k], b[k])

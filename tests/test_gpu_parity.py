@@ -377,6 +377,99 @@ def test_il_epoch_matches_oracle(D, mode):
         wt = torch.tensor(w, device=dev)
 
 
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_il_epoch_c3_shape_matches_reference(D, mode):
+    """The benched function at the benched shape: docp_il_epoch at C3
+    (random_convex_instance(8,4,100), shared expert w*, max 5 SQP iterations,
+    eps 1e-12) over the first 256 problems of bench.py's batch, two epochs with
+    warm caches, against the reference build's train_il epoch body
+    (oracle/_ref, train.hpp:82-131) on the same inputs. PARITY: every field
+    bit for bit and equal per-instance SQP and PCG counts. FAST: equal SQP
+    counts, PCG counts equal except at a warm start on the exit threshold
+    (one iteration apart), <= 1e-9 relative."""
+    import torch
+    if not po.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    nx, nu, T, B = 8, 4, 100, 256
+    th = D.generate_affine_quadratic(nx, nu, 0, B)
+    assert np.array_equal(th, po.gen_aq(nx, nu, T, 0, B))
+    prob = D.affine_quadratic(nx, nu, T)
+    nz, nl = D.sizes(prob)
+    pp = po.aq_problem(nx, nu, T)
+    expert = th.copy()
+    expert[:, :nx] = np.array([1, 2, 1.5, 1, 1, 2, 1.5, 1.0])
+    demos = np.array([po.Oracle("ref", pp).sqp_solve(expert[j], np.zeros(nz), np.zeros(nl), po.sqp_config()).z
+                      for j in range(B)])
+    w = po.gen_uniform(0, nx)
+    cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode=mode))
+    b = D.Batch(prob, B)
+    b.upload(D._lib.F_THETA, th)
+    b.upload(D._lib.F_LAMBDA, np.zeros((B, nl)))
+    b.upload(D._lib.F_LAMBDA_TILDE, np.zeros((B, nl)))
+    dev = torch.device("cuda")
+    demos_t = torch.tensor(demos, device=dev)
+    out_t = torch.zeros(1 + nx, dtype=torch.float64, device=dev)
+    lam_c, lt_c = np.zeros((B, nl)), np.zeros((B, nl))
+    count_diffs = 0
+    for epoch in range(2):
+        wt = torch.tensor(w, device=dev)
+        b.il_epoch(cfg, wt.data_ptr(), 0, nx, demos_t.data_ptr(), float(B), out_t.data_ptr(),
+                   out_t.data_ptr() + 8)
+        b.il_check(epoch)
+        th_e = th.copy()
+        th_e[:, :nx] = w
+        loss, grad, losses, grads, sqp_it, pcg_it = po.il_epoch("ref", pp, th_e, demos, lam_c, lt_c,
+                                                                 po.sqp_config(max_sqp_iters=5), 0, nx)
+        g_sqp = b.download(D._lib.F_SQP_ITERS).ravel()
+        hist = b.download(D._lib.F_PCG_HISTORY)
+        g_pcg = np.array([hist[j, :g_sqp[j]].sum() for j in range(B)]) + b.download(D._lib.F_PCG_ITERS).ravel()
+        out = out_t.cpu().numpy()
+        assert np.array_equal(g_sqp, sqp_it), "SQP iteration counts"
+        if mode == "parity":
+            assert np.array_equal(g_pcg, pcg_it), "PCG iteration counts"
+            assert out[0] == loss and np.array_equal(out[1:], grad)
+            assert np.array_equal(b.download(D._lib.F_LOSS).ravel(), losses)
+            assert np.array_equal(b.download(D._lib.F_LAMBDA), lam_c)
+            assert np.array_equal(b.download(D._lib.F_LAMBDA_TILDE), lt_c)
+        else:
+            d = np.abs(g_pcg - pcg_it)
+            count_diffs += int(np.sum(d != 0))
+            assert d.max() <= 1
+            assert abs(out[0] - loss) <= RTOL_FAST * max(1.0, abs(loss))
+            assert rel(out[1:], grad) <= RTOL_FAST
+            assert rel(b.download(D._lib.F_LAMBDA), lam_c) <= RTOL_FAST
+            assert rel(b.download(D._lib.F_LAMBDA_TILDE), lt_c) <= RTOL_FAST
+        w = w - 1e-2 * grad
+    print(f"{mode}: instances whose PCG total differs from the reference by one: {count_diffs} of {2 * B}")
+    assert count_diffs <= 2
+
+
+def test_il_epoch_failed_demonstration_is_reported(D):
+    """A demonstration whose solve throws fails the epoch as train_il does
+    (train.hpp:111-119): it contributes nothing to the sums, is counted on the
+    device, and il_check raises "epoch E, demonstration J: <reference message>"."""
+    import torch
+    nx, nu, T, B = 4, 2, 10, 4
+    prob = D.affine_quadratic(nx, nu, T)
+    nz, nl = D.sizes(prob)
+    th = D.generate_affine_quadratic(nx, nu, 0, B)
+    th[2, nx + nu] = np.nan  # A(0, 0) of instance 2: non-finite dynamics at stage 0
+    cfg = D.SqpConfig(max_sqp_iters=3, pcg=D.PcgConfig(mode="parity"))
+    b = D.Batch(prob, B)
+    b.upload(D._lib.F_THETA, th)
+    dev = torch.device("cuda")
+    demos = torch.zeros((B, nz), dtype=torch.float64, device=dev)
+    w = torch.full((nx,), 0.5, dtype=torch.float64, device=dev)
+    out = torch.zeros(1 + nx, dtype=torch.float64, device=dev)
+    b.il_epoch(cfg, w.data_ptr(), 0, nx, demos.data_ptr(), float(B), out.data_ptr(), out.data_ptr() + 8)
+    with pytest.raises(D.EvaluationError, match=r"^epoch 3, demonstration 2: .*non-finite"):
+        b.il_check(3)
+    assert np.isfinite(out.cpu().numpy()).all()
+    losses = b.download(D._lib.F_LOSS).ravel()
+    assert out[0].item() == ((0.0 + losses[0]) + losses[1]) + losses[3]
+    assert b.il_failures() == (0, -1)  # reset by the check
+
+
 @pytest.mark.parametrize("nx,nu,T", [(4, 2, 10), (8, 4, 30)])
 def test_error_statuses(D, nx, nu, T):
     """Per-problem failures become the reference's errors; the rest of the

@@ -1,19 +1,52 @@
-"""One PCG launch at C3 shape with a fixed iteration cap (for ncu)."""
-import os, sys
+"""One batched PCG launch with a fixed iteration count on blocks assembled from
+random_convex_instance draws (for ncu and clock studies of K2 alone).
+
+  python tools/pcg_one.py [--nx 8 --nu 4 --T 100 --B 1184 --iters 41 --mode fast|parity]
+"""
+import argparse
+import os
+import sys
+
 import numpy as np
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import paper_2510_06179_b200 as D
-from paper_2510_06179_b200 import _lib as L
-B, T, iters = 1184, 100, int(sys.argv[1]) if len(sys.argv) > 1 else 41
-prob = D.affine_quadratic(8, 4, T)
+import paper_2510_06179_b200 as D  # noqa: E402
+from paper_2510_06179_b200 import _lib as L  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--nx", type=int, default=8)
+ap.add_argument("--nu", type=int, default=4)
+ap.add_argument("--T", type=int, default=100)
+ap.add_argument("--B", type=int, default=1184)
+ap.add_argument("--iters", type=int, default=41)
+ap.add_argument("--mode", default="fast")
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+prob = D.affine_quadratic(a.nx, a.nu, a.T)
 nz, nl = D.sizes(prob)
-b = D.Batch(prob, B)
-b.upload(L.F_THETA, D.generate_affine_quadratic(8, 4, 0, B))
-b.upload(L.F_Z, np.zeros((B, nz)))
-b.linearize(); b.assemble_schur(); b.assemble_gamma()
-for rep in range(3):
-    b.upload(L.F_LAMBDA, np.zeros((B, nl)))
-    b.pcg_solve(D.PcgConfig(epsilon=1e-300, max_iters=iters, mode="fast"))
-b.sync()
-print("ok")
+b = D.Batch(prob, a.B)
+b.upload(L.F_THETA, D.generate_affine_quadratic(a.nx, a.nu, 0, a.B))
+b.upload(L.F_Z, np.zeros((a.B, nz)))
+b.linearize()
+b.assemble_schur()
+b.assemble_gamma()
+b.profile_begin()
+for rep in range(a.reps):
+    b.upload(L.F_LAMBDA, np.zeros((a.B, nl)))
+    b.pcg_solve(D.PcgConfig(epsilon=1e-300, max_iters=a.iters, mode=a.mode))
+prof = b.profile_end()
+ms = prof["kernels"]["pcg"]["ms"] / a.reps
+print(f"{D.describe(prob)} B={a.B} mode={a.mode}: {ms:.3f} ms per launch of {a.iters} iterations, "
+      f"{ms * 1e6 / a.iters / max(1, -(-a.B // 148)):.0f} ns per iteration per problem wave")
+if hasattr(L.lib(), "docp_h8p_clock"):  # A/B build with -DDOCP_H8P_CLOCK
+    import ctypes as C
+    buf = (C.c_ulonglong * 12)()
+    L.lib().docp_h8p_clock(buf)
+    its = a.iters * a.reps * -(-a.B // 148)  # iterations seen by CTA 0's thread 0 (approx.)
+    names = ["S phase1", "barrier", "S phase2", "P phase2", "P phase1", "-", "dot partial", "dot barrier",
+             "chain+bcast", "alpha/beta/updates", "loop exit", "setup"]
+    tot = sum(buf)
+    for k in range(12):
+        if buf[k]:
+            print(f"  {names[k]:20s} {buf[k] / 148 / its:8.0f} cycles/iter  {100 * buf[k] / tot:5.1f}%")
