@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
     ap.add_argument("--no-parity-pass", action="store_true",
                     help="skip the PARITY-mode pass and the FAST/PARITY iteration-count tally")
+    ap.add_argument("--no-fp32-pass", action="store_true", help="skip the fp32-mode pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU time of the baseline sample")
     return ap.parse_args()
@@ -501,7 +502,7 @@ def run_ours(args):
         epoch()
         cf = counts()
         restore(state0)
-        epoch(c=pcfg)
+        tot_p = epoch(c=pcfg).clone()  # [loss | grad] of the first epoch, reference bits
         cp = counts()
         fwd_diff = int(sum(np.sum(cf[1][j, :cp[0][j]] != cp[1][j, :cp[0][j]]) for j in range(B)))
         tally = {"instances": B, "sqp_count_mismatches": int(np.sum(cf[0] != cp[0])),
@@ -526,6 +527,35 @@ def run_ours(args):
                   "note": "PARITY mode: no FMA contraction, reference fold orders (btd_matvec diag->sub->super, "
                           "block_dot in block-index order); bit-identical to the reference build",
                   "count_tally_vs_parity": tally}
+
+    # fp32 mode (pcg_kernel_h8x: fp32 blocks and iterates, relative eps 1e-6;
+    # K1/K3/K4 fp64) over the same epochs; its first epoch against PARITY's
+    fp32 = None
+    if args.mode == "fast" and not args.no_fp32_pass and not args.no_parity_pass:
+        fcfg = D.SqpConfig(max_sqp_iters=5, convergence_tol=1e-4, pcg=D.PcgConfig(epsilon=1e-6, mode="fp32"))
+        restore(state0)
+        tot_f = epoch(c=fcfg).clone()
+        sqp_f = b.download(L.F_SQP_ITERS).ravel().copy()
+        restore(state0)
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(args.steps):
+            epoch(c=fcfg)
+        q1.record(stream)
+        barrier()
+        b.il_check()
+        fms = max_over_ranks(q0.elapsed_time(q1), dev)
+        fv = global_batch * args.steps / (fms / 1e3)
+        a, r = tot_f.cpu().numpy(), tot_p.cpu().numpy()
+        fp32 = {"value": fv, "unit": "problems/s", "ms_per_step": fms / args.steps,
+                "ratio_to_benched_mode": fv / value, "dtype": "f32 (K2 blocks and iterates; dots, K1/K3/K4 f64)",
+                "config": {"pcg_epsilon_relative": 1e-6, "sqp_convergence_tol": 1e-4},
+                "first_epoch_sqp_counts_equal_parity": int(np.sum(sqp_f == cp[0])),
+                "first_epoch_vs_parity": {"loss_rel": abs(a[0] - r[0]) / abs(r[0]),
+                                          "grad_rel": float(np.linalg.norm(a[1:] - r[1:]) / np.linalg.norm(r[1:]))},
+                "stated_bound": "z, lambda, lambda~, theta-gradient within 1e-4 relative of the fp64 reference "
+                                "(tests/test_gpu_fp32.py)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -562,6 +592,7 @@ def run_ours(args):
                          "smem_peak_derived": smem_peak, "frac_smem": achieved / smem_peak},
             "cpu_baseline": cpu,
             "parity_mode": parity,
+            "fp32_mode": fp32,
             "e2e": {"value": e2e_value, "unit": "problems/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "loss_last": host_results[-1][0], "same_epochs_as_timed": host_results[-1][0] == loss_last},
             "clocks": clocks.summary(),

@@ -111,7 +111,14 @@ typedef struct docp_problem {
 
 /* PCG arithmetic: PARITY reproduces the reference's operation order
  * (sequential folds, no FMA) bit for bit; FAST uses FMA and tree reductions. */
-enum docp_pcg_mode { DOCP_PCG_FAST = 0, DOCP_PCG_PARITY = 1 };
+/* FAST: fp64, FMA and tree reductions inside K2 (<= 1e-9 of the reference).
+ * PARITY: fp64, the reference's operation order bit for bit.
+ * FP32: K2 on fp32 blocks and iterates (dots and scalars fp64), n_x = 8;
+ *       K1/K3/K4 stay fp64. epsilon is RELATIVE in this mode: the solve stops
+ *       at eta <= epsilon^2 * gamma' Phi^-1 gamma (an absolute 1e-12 is below
+ *       fp32 resolution). Stated bound: z, lambda, lambda~ and the theta-
+ *       gradient within 1e-4 relative of the fp64 reference at epsilon = 1e-6. */
+enum docp_pcg_mode { DOCP_PCG_FAST = 0, DOCP_PCG_PARITY = 1, DOCP_PCG_FP32 = 2 };
 
 typedef struct docp_pcg_config { /* PcgConfig, pcg.hpp:7-23 */
   double epsilon;                /* exit when eta = r'r~ <= epsilon^2 */

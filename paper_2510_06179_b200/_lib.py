@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("DOCP_LIB_PATH") or os.path.join(HERE, "lib", "libdocp
 
 AFFINE_QUADRATIC, CARTPOLE, ATTITUDE = 1, 2, 3
 OK, DIMENSION, EVALUATION, NUMERICAL, BREAKDOWN, DIVERGENCE, UNSUPPORTED, CUDA_ERROR, INVALID = range(9)
-PCG_FAST, PCG_PARITY = 0, 1
+PCG_FAST, PCG_PARITY, PCG_FP32 = 0, 1, 2
 RHS_FORWARD, RHS_ADJOINT = 0, 1
 MAX_STEP_CANDIDATES = 8
 

@@ -111,7 +111,10 @@ class PcgConfig:
     mode: str = "fast"
 
     def c(self) -> L.PcgConfigC:
-        return L.PcgConfigC(self.epsilon, self.max_iters, L.PCG_PARITY if self.mode == "parity" else L.PCG_FAST)
+        modes = {"fast": L.PCG_FAST, "parity": L.PCG_PARITY, "fp32": L.PCG_FP32}
+        if self.mode not in modes:
+            raise ValueError(f"PcgConfig.mode must be one of {sorted(modes)}, not {self.mode!r}")
+        return L.PcgConfigC(self.epsilon, self.max_iters, modes[self.mode])
 
 
 @dataclass

@@ -143,6 +143,9 @@ int h8s_variant_for(const docp_dev::Dims& d, int device);
 /// pcg_kernel_h8p (PARITY) variant for a device-assembled system (0: none; 1: prefetching; 2: no prefetch).
 int h8p_variant_for(const docp_dev::Dims& d, int device);
 DOCP_PCG_LAUNCHER(launch_pcg_nx8);
+/// The fp32 mode's K2 (pcg_kernel_h8x, n_x = 8).
+int launch_pcg_fp32_nx8(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
+                        int max_iters);
 DOCP_PCG_LAUNCHER(launch_pcg_nxrt);
 
 }  // namespace docp_host

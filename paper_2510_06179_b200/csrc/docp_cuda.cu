@@ -256,6 +256,11 @@ PcgPlan plan_pcg(const docp_batch* b) {
 int launch_pcg(docp_batch* b, const docp_pcg_config& cfg, const int* list, const int* count, int n_hint,
                double* sol) {
   if (!(cfg.epsilon > 0.0 && cfg.max_iters >= 0)) return fail(DOCP_DIMENSION, "pcg: invalid config");
+  if (cfg.mode == DOCP_PCG_FP32) {
+    if (b->d.nx != 8) return fail(DOCP_UNSUPPORTED, "pcg fp32 mode: n_x = 8 only (n_x = %d)", b->d.nx);
+    return launch_pcg_fp32_nx8(b, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+  }
+  if (cfg.mode != DOCP_PCG_FAST && cfg.mode != DOCP_PCG_PARITY) return fail(DOCP_INVALID, "pcg: unknown mode %d", cfg.mode);
   const bool par = cfg.mode == DOCP_PCG_PARITY;
   const PcgPlan pl = plan_pcg(b);
   switch (b->d.nx) {
@@ -723,7 +728,7 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
     const int* list = b->list[cur];
     const int* cnt = b->counts + 1 + cur;
     const int schur = iter == 0 || !keep_blocks;
-    if ((rc = launch_assemble(b, list, cnt, n_bound, cfg->eps_pd, schur, cfg->pcg.mode == DOCP_PCG_FAST))) return rc;
+    if ((rc = launch_assemble(b, list, cnt, n_bound, cfg->eps_pd, schur, cfg->pcg.mode != DOCP_PCG_PARITY))) return rc;
     if ((rc = launch_gamma(b, list, cnt, n_bound, DOCP_RHS_FORWARD))) return rc;
     if ((rc = launch_pcg(b, cfg->pcg, list, cnt, n_bound, b->v.lam))) return rc;
     if ((rc = launch_recover(b, list, cnt, n_bound, b->v.lam, DOCP_RHS_FORWARD))) return rc;
@@ -747,7 +752,7 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
   // every problem of fin was in the first iteration's list (init_solve lists
   // exactly the OK problems; statuses never return to OK)
   const int schur = !(keep_blocks && ran > 0);
-  if ((rc = launch_assemble(b, fin, fin_cnt, b->B, cfg->eps_pd, schur, cfg->pcg.mode == DOCP_PCG_FAST))) return rc;
+  if ((rc = launch_assemble(b, fin, fin_cnt, b->B, cfg->eps_pd, schur, cfg->pcg.mode != DOCP_PCG_PARITY))) return rc;
   if ((rc = launch_kkt(b, fin, fin_cnt, b->B))) return rc;
   return DOCP_OK;
 }
@@ -880,7 +885,7 @@ int docp_rollout_backward(docp_batch* b, const docp_pcg_config* cfg) {
       rollout_back_pre_kernel<<<g, 256, 0, b->stream>>>(b->v, b->roll, t, b->list[0], b->counts + 1);
       LAUNCH_CHECK();
       // the step's cached matrices: re-linearised at its recorded solution
-      if ((rc = launch_assemble(b, b->list[0], b->counts + 1, b->B, b->roll_eps_pd, 1, cfg->mode == DOCP_PCG_FAST)))
+      if ((rc = launch_assemble(b, b->list[0], b->counts + 1, b->B, b->roll_eps_pd, 1, cfg->mode != DOCP_PCG_PARITY)))
         return rc;
       if ((rc = docp_backward_vjp(b, cfg))) return rc;
       rollout_back_post_kernel<<<grid_for(b->B, 128, b->num_sms * 4), 128, 0, b->stream>>>(b->v, b->roll, t);
@@ -909,13 +914,13 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
   LAUNCH_CHECK();
   if ((rc = docp_sqp_solve(b, cfg))) return rc;
   {
-    auto kl = cfg->pcg.mode == DOCP_PCG_FAST ? il_loss_kernel<true> : il_loss_kernel<false>;
+    auto kl = cfg->pcg.mode != DOCP_PCG_PARITY ? il_loss_kernel<true> : il_loss_kernel<false>;
     kl<<<grid_for(static_cast<long>(b->B) * 32, kIlLossThreads, b->num_sms * 8), kIlLossThreads, 0, b->stream>>>(
         b->v, demos, den);
   }
   LAUNCH_CHECK();
   if ((rc = docp_backward_vjp(b, &cfg->pcg))) return rc;
-  if (cfg->pcg.mode == DOCP_PCG_FAST) {
+  if (cfg->pcg.mode != DOCP_PCG_PARITY) {
     il_sum_tree_kernel<<<1 + learn_size, kIlTreeThreads, 0, b->stream>>>(b->v, learn_start, loss_sum, grad_sum,
                                                                         b->counts + 4);
   } else {

@@ -7,6 +7,7 @@
 #include "k_pcg_h8p.cuh"
 #include "k_pcg_h8r.cuh"
 #include "k_pcg_h8s.cuh"
+#include "k_pcg_h8x.cuh"
 #include "pcg_launch.cuh"
 
 namespace docp_host {
@@ -132,6 +133,26 @@ static int launch_h8p(docp_batch* b, const int* list, const int* count, int n_hi
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   if (per_sm < 1) return -1;
+  const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
+  CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
+  ProfScope ps(b, DOCP_PROF_PCG);
+  kern<<<grid, threads, smem, b->stream>>>(b->v, list, count, b->counts + 3, sol, eps, max_iters);
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+/// fp32 mode (n_x = 8): pcg_kernel_h8x, two CTAs per SM up to T = 127, one
+/// beyond (T <= 255).
+int launch_pcg_fp32_nx8(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
+                        int max_iters) {
+  const int threads = (2 * b->d.nb + 31) / 32 * 32;
+  if (threads > 512) return fail(DOCP_UNSUPPORTED, "pcg fp32 mode: horizon %d too long (T <= 255)", b->d.T);
+  auto kern = threads <= 256 ? pcg_kernel_h8x<256> : pcg_kernel_h8x<512>;
+  const size_t smem = h8x_smem_bytes(b->d, threads);
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) return fail(DOCP_UNSUPPORTED, "pcg fp32 mode: kernel does not fit on an SM (smem %zu)", smem);
   const int grid = std::max(1, std::min(n_hint, per_sm * b->num_sms));
   CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
   ProfScope ps(b, DOCP_PROF_PCG);
