@@ -37,6 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "OCP solve+gradient problems/sec (batch 4096, T=100) at 1/2/4/8 B200; PCG HBM %"
+METRIC_C4 = "C4 drifting OCP solve+gradient problems/sec (batch 65536 split over the GPUs, T=100)"
 NX, NU, T = 8, 4, 100
 EXPERT_W = np.array([1.0, 2.0, 1.5, 1.0, 1.0, 2.0, 1.5, 1.0])  # shared expert weights
 LR = 1e-2                                                     # IlTrainOptions (train.hpp:38-46)
@@ -48,7 +49,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=4096,
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
+                    help="c3: the headline IL batch (BASELINE.json); c4: the drifting family "
+                         "(SURVEY.md §8(f)5), 65,536 domain-randomised problems split over the GPUs")
+    ap.add_argument("--batch", type=int, default=None,
                     help="problems per GPU (weak scaling) or in total (strong scaling)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: --batch problems per GPU; strong: --batch problems split over the GPUs")
@@ -316,7 +320,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
 
-    prob = D.affine_quadratic(NX, NU, T)
+    c4 = args.workload == "c4"
+    prob = D.drift(T, 0.1) if c4 else D.affine_quadratic(NX, NU, T)
     nz, nl = D.sizes(prob)
     nth = D.theta_size(prob)
     # this rank's contiguous shard of one sequential draw (generators.hpp:102-111):
@@ -326,12 +331,13 @@ def run_ours(args):
     B = hi - lo
     if B < 1:
         raise SystemExit(f"rank {rank}: empty shard ({global_batch} problems over {world} ranks)")
-    th_all = D.generate_affine_quadratic(NX, NU, 0, global_batch)
+    th_all = D.drift_thetas(global_batch, seed=0) if c4 else D.generate_affine_quadratic(NX, NU, 0, global_batch)
     thetas = th_all[lo:hi].copy()
 
     # expert demonstrations: sqp_solve at theta* (default SqpConfig), on the GPU, untimed
     expert = thetas.copy()
-    expert[:, :NX] = EXPERT_W
+    if not c4:
+        expert[:, :NX] = EXPERT_W
     b = D.Batch(prob, B, local)
     b.set_stream(stream.cuda_stream)
     b.upload(L.F_THETA, expert)
@@ -345,7 +351,9 @@ def run_ours(args):
     demos = torch.tensor(demos_host, device=dev)
 
     # training state: learned shared weights ~ U[0,1]^8 (train.hpp:61-64), caches zero
-    w = torch.tensor(D.generate_uniform(0, NX), device=dev)
+    w0 = D.generate_uniform(0, NX, 0.5, 1.5) * D.api.DRIFT_W_X if c4 else D.generate_uniform(0, NX)
+    w = torch.tensor(w0, device=dev)
+    lr = LR
     b.upload(L.F_THETA, thetas)
     b.upload(L.F_LAMBDA, np.zeros((B, nl)))
     b.upload(L.F_LAMBDA_TILDE, np.zeros((B, nl)))
@@ -357,7 +365,11 @@ def run_ours(args):
         dptr = (demos if demo_buf is None else demo_buf).data_ptr()
         b.il_epoch(c, w.data_ptr(), 0, NX, dptr, den, out.data_ptr(), out.data_ptr() + 8)
         tot = fixed_order_allreduce(out) if world > 1 else out
-        w.sub_(LR * tot[1:])
+        if c4:  # positive weights, gradients spanning 1e-3..1e7: an exponentiated-gradient step (<= 5% per epoch)
+            gw = tot[1:] * w
+            w.mul_(torch.exp(-0.05 * gw / gw.abs().max().clamp_min(1e-300)))
+        else:
+            w.sub_(lr * tot[1:])
         return tot
 
     def barrier():
@@ -558,7 +570,7 @@ def run_ours(args):
                                 "(tests/test_gpu_fp32.py)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not c4:
         try:
             cpu = measure_cpu_baseline(args.cpu_seconds)
         except Exception as exc:  # reported, never fatal
@@ -567,15 +579,21 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC_C4 if c4 else METRIC, "value": value, "unit": "problems/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: random_convex_instance(8,4,100) draws (reference recipe, mt19937_64 seed 0), "
-                    "expert demonstrations solved on the GPU at w*",
-            "config": {"workload": "C3 imitation-learning epoch (train_il body): solve + adjoint gradient + "
-                                   "fixed-order sum + theta-gradient exchange + GD step",
-                       "batch_per_gpu": B, "global_batch": global_batch, "horizon": T, "n_x": NX, "n_u": NU,
+            "data": ("synthetic: domain-randomised drifting instances (drift_thetas, +-10% vehicle parameters, "
+                     "numpy seed 0), expert demonstrations solved on the GPU at the nominal weights; the model "
+                     "has no reference implementation (SURVEY.md §8(f)5)") if c4 else
+                    ("synthetic: random_convex_instance(8,4,100) draws (reference recipe, mt19937_64 seed 0), "
+                     "expert demonstrations solved on the GPU at w*"),
+            "config": {"workload": ("C4 drifting family (dynamic bicycle + Fiala tires, n_x 8, n_u 2, T 100) "
+                                    "imitation-learning epoch") if c4 else
+                                   ("C3 imitation-learning epoch (train_il body): solve + adjoint gradient + "
+                                    "fixed-order sum + theta-gradient exchange + GD step"),
+                       "batch_per_gpu": B, "global_batch": global_batch, "horizon": T, "n_x": NX,
+                       "n_u": 2 if c4 else NU,
                        "max_sqp_iters": 5, "pcg_epsilon": 1e-12, "pcg_mode": args.mode,
                        "parallelism": f"dp{world} (instance sharding)",
                        "l2": "inputs larger than L2: %.0f MB of Schur blocks per GPU" %
@@ -626,6 +644,10 @@ def spawn_command(args, argv):
 
 def main():
     args = parse()
+    if args.batch is None:
+        args.batch = 4096 if args.workload == "c3" else 65536
+    if args.workload == "c4":
+        args.scaling = "strong"
     world = os.environ.get("WORLD_SIZE")
     if world is None and args.gpus > 1:
         return subprocess.call(spawn_command(args, sys.argv[1:]))

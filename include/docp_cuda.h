@@ -59,7 +59,12 @@ extern "C" {
  * docp_problem.dt. Its per-instance AttitudeParams::inertia rides in THETA's
  * tail: THETA = [w_x 3 | w_u 3 | omega_0 3 | inertia 3] (the reference's 9
  * entries, make_attitude_theta, then the inertia); GRAD_THETA's inertia tail is 0. */
-enum docp_family { DOCP_AFFINE_QUADRATIC = 1, DOCP_CARTPOLE = 2, DOCP_ATTITUDE = 3 };
+/* DOCP_DRIFT (include/docp_drift_model.h; no reference implementation exists,
+ * SURVEY.md §8(f)5): dynamic bicycle with Fiala tires, n_x = 8, n_u = 2, cost
+ * scale 0.5, Heun steps over docp_problem.dt; THETA = [w_x 8 | w_u 2 |
+ * xbar_0 8 | X_ref 8 | vehicle parameters 10] (36); GRAD_THETA covers the first
+ * 18 entries (make_quadratic_cost_theta_vjp), the tail is 0. */
+enum docp_family { DOCP_AFFINE_QUADRATIC = 1, DOCP_CARTPOLE = 2, DOCP_ATTITUDE = 3, DOCP_DRIFT = 4 };
 
 /* docp::Error hierarchy (common.hpp:18-54) plus ABI-level failures. */
 enum docp_code {
@@ -106,7 +111,7 @@ typedef struct docp_problem {
   int32_t n_x, n_u, horizon;
   double cost_scale;                             /* affine-quadratic (affine_quadratic.hpp:25) */
   double cart_mass, pole_mass, length, gravity;  /* cart-pole (cartpole.hpp:17-26) */
-  double dt;                                     /* cart-pole and attitude time step */
+  double dt;                                     /* cart-pole, attitude and drift time step */
 } docp_problem;
 
 /* PCG arithmetic: PARITY reproduces the reference's operation order

@@ -21,7 +21,8 @@
 extern "C" {
 #endif
 
-enum { PORT_AFFINE_QUADRATIC = 1, PORT_CARTPOLE = 2, PORT_ATTITUDE = 3 /* ref build only */ };
+enum { PORT_AFFINE_QUADRATIC = 1, PORT_CARTPOLE = 2, PORT_ATTITUDE = 3 /* ref build only */,
+       PORT_DRIFT = 4 /* ref build only: the reference solver on include/docp_drift_model.h */ };
 enum {
   PORT_OK = 0,
   PORT_DIMENSION = 1,

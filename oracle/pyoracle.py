@@ -23,7 +23,7 @@ LIBS = {
     "ref": os.path.join(HERE, "_ref", "libdocp_ref.so"),
 }
 
-AFFINE_QUADRATIC, CARTPOLE, ATTITUDE = 1, 2, 3
+AFFINE_QUADRATIC, CARTPOLE, ATTITUDE, DRIFT = 1, 2, 3, 4
 CODES = {0: "OK", 1: "DIMENSION", 2: "EVALUATION", 3: "NUMERICAL", 4: "BREAKDOWN", 5: "DIVERGENCE", 99: "ERROR"}
 
 
@@ -81,7 +81,15 @@ def attitude_problem(T=25, inertia=(1.0, 1.0, 1.0), dt=0.1) -> Problem:
     return p
 
 
+def drift_problem(T=100, dt=0.1) -> Problem:
+    """The drifting family (include/docp_drift_model.h; ref build only: the
+    reference solver on the shared model definition)."""
+    return Problem(DRIFT, 8, 2, T, 0.5, 0.0, 0.0, 0.0, 0.0, dt)
+
+
 def theta_size(p: Problem) -> int:
+    if p.family == DRIFT:
+        return 36
     if p.family in (CARTPOLE, ATTITUDE):
         return 2 * p.nx + p.nu
     return p.nx + p.nu + p.nx * p.nx + p.nx * p.nu + 2 * p.nx
@@ -160,6 +168,8 @@ def load(kind: str):
             lib.ref_train_il_cartpole.restype = C.c_int
             lib.ref_train_il_cartpole.argtypes = [C.c_uint64, C.c_int, C.c_int, dp, C.c_int, C.c_double, dp,
                                                   C.POINTER(C.c_long), C.POINTER(C.c_long), dp, sp]
+            lib.ref_drift_step.restype = None
+            lib.ref_drift_step.argtypes = [dp, C.c_double, dp, dp, dp, dp, dp]
             lib.ref_gen_uniform.restype = None
             lib.ref_gen_uniform.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, dp]
             lib.ref_spectral_radius.restype = C.c_double

@@ -16,6 +16,10 @@
 #include <memory>
 
 #include "port/docp_port.h"
+// The drifting family has no reference implementation: its
+// single model definition is shared with the GPU path, so this harness runs
+// the REFERENCE solver (sqp_solve / backward_vjp / train_il body) on it.
+#include "docp_drift_model.h"
 
 using namespace docp;
 
@@ -60,6 +64,28 @@ void put(const Matrix& m, double* out) {
 /// Family -> OcpDefinition. AffineQuadratic reads every coefficient from
 /// theta (affine_quadratic.hpp:39-81), so the struct only carries sizes.
 OcpDefinition make_ocp(const port_problem& p) {
+  if (p.family == PORT_DRIFT) {  // the cart-pole pattern (cartpole.hpp:91-107) on the shared drift model
+    OcpDefinition ocp;
+    ocp.n_x = docp_drift::NX;
+    ocp.n_u = docp_drift::NU;
+    ocp.horizon = p.horizon;
+    ocp.state_cost = make_diag_quadratic_cost(segment::state_cost, 0.5);
+    ocp.control_cost = make_diag_quadratic_cost(segment::control_cost, 0.5);
+    const double dt = p.dt;
+    ocp.dynamics_residual = make_explicit_dynamics(
+        [dt](int, const Vector& x, const Vector& u, const ParameterVector& theta) {
+          const Vector th = theta.values();
+          ExplicitStep s;
+          s.x_next = Vector::Zero(docp_drift::NX);
+          s.jac_x = Matrix::Zero(docp_drift::NX, docp_drift::NX);
+          s.jac_u = Matrix::Zero(docp_drift::NX, docp_drift::NU);
+          docp_drift::step(th.data(), dt, x.data(), u.data(), s.x_next.data(), s.jac_x.data(), s.jac_u.data());
+          return s;
+        });
+    ocp.initial_state = [](const ParameterVector& theta) { return Vector(theta.segment(segment::initial_state)); };
+    ocp.theta_vjp = make_quadratic_cost_theta_vjp(0.5);
+    return ocp;
+  }
   if (p.family == PORT_ATTITUDE) {
     AttitudeParams ap;
     ap.inertia = vec(p.inertia, 3);
@@ -97,6 +123,11 @@ ParameterVector make_theta(const port_problem& p, const double* th) {
     seg(segment::state_cost, p.nx);
     seg(segment::control_cost, p.nu);
     seg(segment::initial_state, p.nx);
+  } else if (p.family == PORT_DRIFT) {
+    seg(segment::state_cost, p.nx);
+    seg(segment::control_cost, p.nu);
+    seg(segment::initial_state, p.nx);
+    seg("drift_model", docp_drift::NTH - docp_drift::TH_XREF);  // X_ref + vehicle parameters
   } else {
     seg(segment::state_cost, p.nx);
     seg(segment::control_cost, p.nu);
@@ -370,7 +401,8 @@ int ref_il_epoch(const port_problem* p, int batch, const double* thetas, const d
   clear(st);
   OcpDefinition ocp = make_ocp(*p);
   SqpConfig cfg = make_cfg(*c);
-  const int nth = (p->family == PORT_CARTPOLE || p->family == PORT_ATTITUDE)
+  const int nth = p->family == PORT_DRIFT ? docp_drift::NTH
+                  : (p->family == PORT_CARTPOLE || p->family == PORT_ATTITUDE)
                       ? 2 * p->nx + p->nu
                       : p->nx + p->nu + p->nx * p->nx + p->nx * p->nu + 2 * p->nx;
   const Eigen::Index nz = ocp.primal_size(), nl = ocp.dual_size();
@@ -576,6 +608,12 @@ void ref_gen_uniform(std::uint64_t seed, int n, double lo, double hi, double* ou
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> unit(lo, hi);
   for (int i = 0; i < n; ++i) out[i] = unit(rng);
+}
+
+/// The drifting model's explicit step and Jacobians (include/docp_drift_model.h), host build.
+void ref_drift_step(const double* th, double dt, const double* xbar, const double* u, double* xn, double* jx,
+                    double* ju) {
+  docp_drift::step(th, dt, xbar, u, xn, jx, ju);
 }
 
 /// Reference spectral radius (generators.hpp:41-46) of an n x n col-major matrix.

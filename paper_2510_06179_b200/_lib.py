@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DOCP_LIB_PATH") or os.path.join(HERE, "lib", "libdocp_cuda.so")  # override: A/B builds
 
-AFFINE_QUADRATIC, CARTPOLE, ATTITUDE = 1, 2, 3
+AFFINE_QUADRATIC, CARTPOLE, ATTITUDE, DRIFT = 1, 2, 3, 4
 OK, DIMENSION, EVALUATION, NUMERICAL, BREAKDOWN, DIVERGENCE, UNSUPPORTED, CUDA_ERROR, INVALID = range(9)
 PCG_FAST, PCG_PARITY, PCG_FP32 = 0, 1, 2
 RHS_FORWARD, RHS_ADJOINT = 0, 1

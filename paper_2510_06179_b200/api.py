@@ -172,6 +172,43 @@ def attitude(horizon: int = 25, dt: float = 0.1) -> L.Problem:
     return L.Problem(L.ATTITUDE, 3, 3, horizon, 0.5, 0.0, 0.0, 0.0, 0.0, dt)
 
 
+# The drifting family (include/docp_drift_model.h). No
+# reference implementation or generator exists. Nominal vehicle: the paper's
+# Table (a, b, m, r_w, C_f, C_r, mu_f, mu_r) plus our I_z and path curvature
+# kappa (a 10 m circle); the reference state is the model's steady cornering
+# equilibrium at 8 m/s on that circle, heading offset -beta so the velocity is
+# tangent to the path (f(X_ref, 0) = 0 to 1e-15 except ds/dt = V, computed with
+# scipy.optimize.fsolve on the model); the weights follow the paper's emphasis
+# on sideslip, heading and lateral error, rescaled so the QPs stay well posed.
+DRIFT_PARAMS = np.array([1.239, 1.209, 1476.0, 2200.0, 0.323, 54000.0, 220000.0, 0.99, 0.90, 0.1])
+DRIFT_REF_STATE = np.array([0.80000000000000004, 8.0, 0.089764022782235914, -0.089764022782235914, 0.0, 0.0,
+                            0.33936077951463062, 0.79350102041864212])
+DRIFT_W_X = np.array([1.0, 0.1, 50.0, 20.0, 30.0, 1e-3, 1.0, 1.0])
+DRIFT_W_U = np.array([10.0, 1.0])
+_DRIFT_X0_SPREAD = np.array([0.05, 0.3, 0.03, 0.05, 0.2, 0.0, 0.02, 0.06])
+
+
+def drift(horizon: int = 100, dt: float = 0.1) -> L.Problem:
+    """Drifting family: n_x = 8 (6 vehicle / path states + steering and drive
+    force), n_u = 2 (their rates), Heun sub-steps over dt. theta = [w_x 8 |
+    w_u 2 | xbar_0 8 | X_ref 8 | a, b, m, I_z, r_w, C_f, C_r, mu_f, mu_r, kappa]."""
+    return L.Problem(L.DRIFT, 8, 2, horizon, 0.5, 0.0, 0.0, 0.0, 0.0, dt)
+
+
+def drift_thetas(count: int, seed: int = 0, spread: float = 0.1, w_x=None, w_u=None) -> np.ndarray:
+    """Domain-randomised drifting instances [count][36]: every vehicle parameter
+    drawn from U(1 - spread, 1 + spread) times nominal, the initial deviation
+    from U(-1, 1) times a per-state scale (numpy PCG64, seeded)."""
+    rng = np.random.default_rng(seed)
+    th = np.zeros((count, 36))
+    th[:, 0:8] = DRIFT_W_X if w_x is None else w_x
+    th[:, 8:10] = DRIFT_W_U if w_u is None else w_u
+    th[:, 10:18] = rng.uniform(-1.0, 1.0, (count, 8)) * _DRIFT_X0_SPREAD
+    th[:, 18:26] = DRIFT_REF_STATE
+    th[:, 26:36] = DRIFT_PARAMS * rng.uniform(1.0 - spread, 1.0 + spread, (count, 10))
+    return th
+
+
 def theta_size(problem: L.Problem) -> int:
     return L.lib().docp_theta_size(C.byref(problem))
 

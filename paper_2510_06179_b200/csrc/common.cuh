@@ -107,7 +107,8 @@ inline Dims make_dims(const docp_problem& p) {
   d.T = p.horizon;
   d.nl = d.nx * (d.T + 1);
   d.nz = d.nl + d.nu * d.T;
-  d.nth = p.family == DOCP_CARTPOLE    ? 9
+  d.nth = p.family == DOCP_DRIFT        ? 36  // docp_drift::NTH
+          : p.family == DOCP_CARTPOLE    ? 9
           : p.family == DOCP_ATTITUDE ? 12  // reference 9 + the instance inertia
                                       : d.nx + d.nu + d.nx * d.nx + d.nx * d.nu + 2 * d.nx;
   d.nb = d.T + 1;

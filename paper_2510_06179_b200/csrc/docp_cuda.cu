@@ -392,7 +392,8 @@ double* field_base(docp_batch* b, int f, size_t* per, size_t* elem) {
 
 int check_problem(const docp_problem* p) {
   if (!p) return fail(DOCP_INVALID, "null problem");
-  if (p->family != DOCP_AFFINE_QUADRATIC && p->family != DOCP_CARTPOLE && p->family != DOCP_ATTITUDE)
+  if (p->family != DOCP_AFFINE_QUADRATIC && p->family != DOCP_CARTPOLE && p->family != DOCP_ATTITUDE &&
+      p->family != DOCP_DRIFT)
     return fail(DOCP_UNSUPPORTED, "unknown problem family %d", p->family);
   if (p->n_x < 1 || p->n_u < 1 || p->horizon < 1) return fail(DOCP_DIMENSION, "dimensions must be positive");
   if (p->n_x > kMaxNx || p->n_u > kMaxNu)
@@ -401,6 +402,8 @@ int check_problem(const docp_problem* p) {
     return fail(DOCP_DIMENSION, "cart-pole has n_x = 4, n_u = 1");
   if (p->family == DOCP_ATTITUDE && (p->n_x != 3 || p->n_u != 3))
     return fail(DOCP_DIMENSION, "attitude has n_x = n_u = 3");
+  if (p->family == DOCP_DRIFT && (p->n_x != 8 || p->n_u != 2))
+    return fail(DOCP_DIMENSION, "drift has n_x = 8, n_u = 2");
   return DOCP_OK;
 }
 
@@ -835,7 +838,7 @@ void key_add(std::vector<char>& k, const T& v) {
 int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init, int32_t x_init_on_device,
                  int32_t H) {
   if (!b || !cfg || !x_init) return fail(DOCP_INVALID, "null argument");
-  if (b->prob.family == DOCP_CARTPOLE)
+  if (b->prob.family == DOCP_CARTPOLE || b->prob.family == DOCP_DRIFT)
     return fail(DOCP_UNSUPPORTED, "rollout: environments exist for the affine and attitude tasks");
   if (H < 1) return fail(DOCP_DIMENSION, "rollout: episode length must be >= 1");
   int rc = validate_sqp(cfg);

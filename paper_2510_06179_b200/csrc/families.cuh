@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 #include "crmath.cuh"
+#include "docp_drift_model.h"
 
 namespace docp_dev {
 
@@ -76,6 +77,16 @@ struct Family {
         for (int k = 0; k < nx * nx; ++k) jx[k] = -a[k];
       if (ju)
         for (int k = 0; k < nx * nu; ++k) ju[k] = -b[k];
+      return;
+    }
+    if (kind == DOCP_DRIFT) {  // make_explicit_dynamics(docp_drift::step): the shared model definition
+      double xn_[docp_drift::NX], jxx[docp_drift::NX * docp_drift::NX], juu[docp_drift::NX * docp_drift::NU];
+      docp_drift::step(th, dt, x, u, xn_, jx ? jxx : nullptr, ju ? juu : nullptr);
+      for (int i = 0; i < docp_drift::NX; ++i) res[i] = xn[i] - xn_[i];
+      if (jx)
+        for (int k = 0; k < docp_drift::NX * docp_drift::NX; ++k) jx[k] = -jxx[k];
+      if (ju)
+        for (int k = 0; k < docp_drift::NX * docp_drift::NU; ++k) ju[k] = -juu[k];
       return;
     }
     if (kind == DOCP_ATTITUDE) {  // make_explicit_dynamics(attitude_step), attitude.hpp:16-42
