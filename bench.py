@@ -56,7 +56,8 @@ def parse():
                     help="problems per GPU (weak scaling) or in total (strong scaling)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: --batch problems per GPU; strong: --batch problems split over the GPUs")
-    ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
+    ap.add_argument("--mode", default="fast", choices=["fast", "parity", "fp32"],
+                    help="PCG arithmetic of the timed pass (fp32: relative eps 1e-6, SQP step tolerance 1e-4)")
     ap.add_argument("--no-parity-pass", action="store_true",
                     help="skip the PARITY-mode pass and the FAST/PARITY iteration-count tally")
     ap.add_argument("--no-fp32-pass", action="store_true", help="skip the fp32-mode pass")
@@ -343,7 +344,7 @@ def run_ours(args):
     b.upload(L.F_THETA, expert)
     b.upload(L.F_Z, np.zeros((B, nz)))
     b.upload(L.F_LAMBDA, np.zeros((B, nl)))
-    b.sqp_solve(D.SqpConfig(pcg=D.PcgConfig(mode=args.mode)))
+    b.sqp_solve(D.SqpConfig(pcg=D.PcgConfig(mode="parity" if args.mode == "parity" else "fast")))  # expert demos (fp64)
     errs = [e for e in b.errors() if e is not None]
     if errs:
         raise RuntimeError(f"expert solves failed: {errs[0]}")
@@ -359,6 +360,8 @@ def run_ours(args):
     b.upload(L.F_LAMBDA_TILDE, np.zeros((B, nl)))
     out = torch.zeros(1 + NX, dtype=torch.float64, device=dev)  # [loss | grad]
     cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode=args.mode))
+    if args.mode == "fp32":
+        cfg = D.SqpConfig(max_sqp_iters=5, convergence_tol=1e-4, pcg=D.PcgConfig(epsilon=1e-6, mode="fp32"))
     den = float(global_batch)
 
     def epoch(demo_buf=None, c=cfg):

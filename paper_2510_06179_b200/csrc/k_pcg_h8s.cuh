@@ -93,7 +93,23 @@ __host__ __device__ inline long h8s_smem_doubles(const Dims& d) {
 /// -S and Phi^-1 halves of a record that does not fit twice in shared memory
 /// are loaded one after the other into the same region. pcg_kernel_h8s_wide
 /// (below) extends that to T <= 191.
-template <int MAXT, bool PREFETCH>
+#ifdef DOCP_H8S_CLOCK
+__device__ unsigned long long g_h8s_clk[12];
+#define H8S_CLK(k)                        \
+  if (tid == 0) {                         \
+    const long long t_ = clock64();       \
+    clk[k] += t_ - t_last;                \
+    t_last = t_;                          \
+  }
+#else
+#define H8S_CLK(k)
+#endif
+
+/// PD_SMEM: the Phi^-1 diagonal blocks are read from shared memory every
+/// iteration (rows 4h..4h+3, as U_i) instead of being held in registers:
+/// 36 registers fewer, for the wide form whose 9-12 warps cap every thread
+/// at 168 registers (an SMSP then holds three warps).
+template <int MAXT, bool PREFETCH, bool PD_SMEM = false>
 __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, const int* __restrict__ n_work,
                                          int* __restrict__ counter, double* __restrict__ sol_all, double epsilon,
                                          int max_iters_cfg) {
@@ -111,6 +127,9 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   const bool has_prev = i > 0;
   const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int nwk = *n_work;
+#ifdef DOCP_H8S_CLOCK
+  long long clk[12] = {0}, t_last = clock64();
+#endif
 
   constexpr int NWS = MAXT <= 256 ? 8 : 16;  // warp slots per dot
   double* sPd = sm_pcg;            // [R] Phi^-1 diagonal blocks (current problem)
@@ -197,8 +216,12 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   };
   auto dot = [&](const double* a, const double* b) -> double {
     partial(a, b, 0);
+    H8S_CLK(6);
     __syncthreads();
-    return total(0);
+    H8S_CLK(7);
+    const double t = total(0);
+    H8S_CLK(8);
+    return t;
   };
   auto norm = [&](const double* a) -> double {
     __syncthreads();
@@ -336,7 +359,9 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       rows_times(so, xf, hand);  // L_i x_i
       put(xbuf, pv0, pv1, hand);  // slot i (see pp0 above)
       partial(a, b, slot);
+      H8S_CLK(0);
       __syncthreads();
+      H8S_CLK(1);
       get(vbuf, nx0, nx1, xn);
       trans_times(so, xn, up);   // L_i' x_{i+1}
       get(xbuf, pp0, pp1, low);
@@ -350,8 +375,16 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       double xf[8], own[4], hand[4], low[4], up[4], xn[8];
       gather(xr, xf);
       put(vbuf, my0, my1, xr);
-      h8s::sym_times(pd, xf, xr, h, own);
+      if constexpr (PD_SMEM) {
+        double2 dd[8][2];
+        h8f::load_rows(PdI, bs, dd);
+        rows_times(dd, xf, own);
+      } else {
+        h8s::sym_times(pd, xf, xr, h, own);
+      }
+      H8S_CLK(3);
       __syncthreads();
+      H8S_CLK(1);
       get(vbuf, nf0, nf1, xn);
       get(vbuf, nf2, nf3, xn + 4);
       {
@@ -361,7 +394,9 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
         rows_times(oo, xn, up);     // U_i x_{i+1}
       }
       put(xbuf, my0, my1, hand);
+      H8S_CLK(4);
       __syncthreads();
+      H8S_CLK(1);
       get(xbuf, pv0, pv1, low);
       finish(own, low, up, out);
     };
@@ -375,7 +410,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     __syncthreads();  // every phase-2 read of lambda / its hand-over is done
     mbar_wait(&s_bar[1], ph1);
     ph1 ^= 1;
-    h8s::load_sym(PdI, ib, h, pd);
+    if constexpr (!PD_SMEM) h8s::load_sym(PdI, ib, h, pd);
     double rt[4], sr[4];  // r~ and (-S) r~
     matvec_p(r, rt);                 // r~ = Phi^-1 r
     // Pipelined second dot: sr = (-S) r~ is formed while eta = r'r~ reduces
@@ -394,6 +429,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
 #pragma unroll
     for (int q = 0; q < 4; ++q) pv[q] = rt[q], y[q] = sr[q];
 
+    H8S_CLK(11);
     while (status == DOCP_OK && eta > threshold && iters < max_iters) {
       const double vv = dot(pv, y);
       if (vv <= 0.0) {
@@ -406,8 +442,11 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
         lam[q] = fma(alpha, pv[q], lam[q]);
         r[q] = fma(-alpha, y[q], r[q]);
       }
+      H8S_CLK(9);
       matvec_p(r, rt);                 // r~
+      H8S_CLK(5);
       matvec_s_dot(rt, sr, r, rt, 1);   // sr = (-S) r~ while eta' = r'r~ reduces
+      H8S_CLK(2);
       double eta_next = total(1);
       if (eta_next < 0.0) {
         const double scale = norm(r) * norm(rt);
@@ -427,6 +466,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       eta = eta_next;
       inv_eta = 1.0 / eta;
       ++iters;
+      H8S_CLK(10);
     }
 
     if (act) {
@@ -445,6 +485,10 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     }
     __syncthreads();  // s_next is published; Phi^-1 / vectors free for the next problem
   }
+#ifdef DOCP_H8S_CLOCK
+  if (tid == 0)
+    for (int k = 0; k < 12; ++k) atomicAdd(&g_h8s_clk[k], static_cast<unsigned long long>(clk[k]));
+#endif
 }
 
 template <int MAXT, bool PREFETCH>
@@ -461,7 +505,7 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
 __global__ void __maxnreg__(168)
     pcg_kernel_h8s_wide(View v, const int* __restrict__ work, const int* __restrict__ n_work,
                         int* __restrict__ counter, double* __restrict__ sol_all, double epsilon, int max_iters_cfg) {
-  h8s_body<384, false>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
+  h8s_body<384, false, true>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
 }
 
 }  // namespace docp_dev

@@ -39,14 +39,20 @@ prof = b.profile_end()
 ms = prof["kernels"]["pcg"]["ms"] / a.reps
 print(f"{D.describe(prob)} B={a.B} mode={a.mode}: {ms:.3f} ms per launch of {a.iters} iterations, "
       f"{ms * 1e6 / a.iters / max(1, -(-a.B // 148)):.0f} ns per iteration per problem wave")
-if hasattr(L.lib(), "docp_h8p_clock"):  # A/B build with -DDOCP_H8P_CLOCK
+for fn in ("docp_h8p_clock", "docp_h8s_clock"):  # A/B builds with -DDOCP_H8P_CLOCK / -DDOCP_H8S_CLOCK
+    if not hasattr(L.lib(), fn):
+        continue
     import ctypes as C
     buf = (C.c_ulonglong * 12)()
-    L.lib().docp_h8p_clock(buf)
+    getattr(L.lib(), fn)(buf)
+    if not sum(buf):
+        continue
     its = a.iters * a.reps * -(-a.B // 148)  # iterations seen by CTA 0's thread 0 (approx.)
-    names = ["S phase1", "barrier", "S phase2", "P phase2", "P phase1", "-", "dot partial", "dot barrier",
-             "chain+bcast", "alpha/beta/updates", "loop exit", "setup"]
+    names = (["S phase1", "barrier", "S phase2", "P phase2", "P phase1", "-", "dot partial", "dot barrier",
+              "chain+bcast", "alpha/beta/updates", "loop exit", "setup"] if fn == "docp_h8p_clock" else
+             ["S phase1 + eta partial", "barriers", "S phase2", "P phase1", "P phase 1b (U)", "P phase2",
+              "dot partial", "dot barrier", "dot total", "alpha + updates", "beta + updates", "setup"])
     tot = sum(buf)
     for k in range(12):
         if buf[k]:
-            print(f"  {names[k]:20s} {buf[k] / 148 / its:8.0f} cycles/iter  {100 * buf[k] / tot:5.1f}%")
+            print(f"  {names[k]:24s} {buf[k] / 148 / its:8.0f} cycles/iter  {100 * buf[k] / tot:5.1f}%")

@@ -8,8 +8,14 @@ from cold caches (lambda = lambda~ = 0, z = 0), CUDA events on the batch
 stream. Reports problems/s, PCG iterations per solve and the PCG kernel's
 algorithmic GB/s (SURVEY.md §8(d) bytes) against the measured HBM peak.
 
+Batches larger than --chunk (default 65,536) run in chunks through one
+device batch of the chunk size: every chunk's thetas are copied in from a
+device-resident array of all B (its own uploads inside the timed region), so
+B = 1M runs in bounded memory (the blocks of 1M problems at T = 256 would
+need 525 GB).
+
 usage: python tools/sweep.py [--T 16,32,64,100,128,256] [--B 1024,4096,16384,65536]
-                             [--reps 3] [--md profiles/r1_sweep.md]
+                             [--reps 3] [--chunk 65536] [--md profiles/r1_sweep.md]
 """
 import argparse
 import json
@@ -43,7 +49,7 @@ def hbm_peak():
 NU = 4
 
 
-def run(T, B, reps, pool_cache):
+def run(T, B, reps, pool_cache, chunk=65536):
     prob = D.affine_quadratic(8, NU, T)
     nz, nl = D.sizes(prob)
     if T not in pool_cache:
@@ -53,21 +59,27 @@ def run(T, B, reps, pool_cache):
     if len(pool) < min(B, POOL):
         pool = pool_cache[T] = D.generate_affine_quadratic(8, NU, 0, min(B, POOL), convex=CONVEX)
     th = np.resize(pool, (B, pool.shape[1])) if B > len(pool) else pool[:B]
-    b = D.Batch(prob, B)
-    b.upload(L.F_THETA, th)
-    g = np.random.default_rng(0).standard_normal((B, nz)) * 1e-2
+    C = min(B, chunk)
+    assert B % C == 0, "the chunk size must divide the batch"
+    b = D.Batch(prob, C)
+    b.set_stream(torch.cuda.current_stream().cuda_stream)
+    th_dev = torch.tensor(th, device="cuda")
+    g = torch.tensor(np.random.default_rng(0).standard_normal((C, nz)) * 1e-2, device="cuda")
     b.upload(L.F_LOSS_GRAD_Z, g)
     cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode="fast"))
-    zeros_z, zeros_l = np.zeros((B, nz)), np.zeros((B, nl))
+    zeros_z = torch.zeros((C, nz), dtype=torch.float64, device="cuda")
+    zeros_l = torch.zeros((C, nl), dtype=torch.float64, device="cuda")
 
     def step():
-        b.upload(L.F_Z, zeros_z)
-        b.upload(L.F_LAMBDA, zeros_l)
-        b.upload(L.F_LAMBDA_TILDE, zeros_l)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        b.sqp_solve(cfg)
-        b.backward_vjp(cfg.pcg)
+        for c0 in range(0, B, C):
+            b.upload(L.F_THETA, th_dev[c0:c0 + C])
+            b.upload(L.F_Z, zeros_z)
+            b.upload(L.F_LAMBDA, zeros_l)
+            b.upload(L.F_LAMBDA_TILDE, zeros_l)
+            b.sqp_solve(cfg)
+            b.backward_vjp(cfg.pcg)
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
@@ -85,7 +97,7 @@ def run(T, B, reps, pool_cache):
             "pcg_iters_per_solve": prof["pcg_iterations"] / max(1, prof["pcg_solves"]),
             "pcg_share": pcg_ms / total_kernel if total_kernel else None, "pcg_algorithmic_GBps": gbs,
             "pcg_frac_hbm": gbs / hbm_peak(), "pcg_kernel": D.describe(prob), "failed_instances": errs,
-            "block_record_MB": B * 16 * 64 * (2 * T + 1) / 1e6}
+            "block_record_MB": B * 16 * 64 * (2 * T + 1) / 1e6, "chunks": B // C}
 
 
 def main():
@@ -94,6 +106,7 @@ def main():
     ap.add_argument("--B", default="1024,4096,16384,65536")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--md", default=None)
+    ap.add_argument("--chunk", type=int, default=65536)
     ap.add_argument("--nu", type=int, default=4)
     ap.add_argument("--convex", action="store_true", help="random_convex_instance draws (domain-randomised weights)")
     a = ap.parse_args()
@@ -103,7 +116,7 @@ def main():
     cache = {}
     for T in [int(x) for x in a.T.split(",")]:
         for B in [int(x) for x in a.B.split(",")]:
-            r = run(T, B, a.reps, cache)
+            r = run(T, B, a.reps, cache, a.chunk)
             rows.append(r)
             print(json.dumps(r), flush=True)
             torch.cuda.empty_cache()
