@@ -97,6 +97,22 @@ inline Family family_of(const CartpoleParams& p) {
   return f;
 }
 
+/// The drifting family (include/docp_drift_model.h; the reference has no
+/// model class for it): theta is the full 36-entry device layout [w_x 8 |
+/// w_u 2 | xbar_0 8 | X_ref 8 | vehicle parameters 10], built by the caller
+/// (e.g. the ParameterVector the reference-solver harness oracle/ref_driver.cpp
+/// uses: segments state_cost, control_cost, initial_state, "drift_model").
+inline Family family_drift(int horizon, double dt) {
+  Family f;
+  f.desc.family = DOCP_DRIFT;
+  f.desc.n_x = 8;
+  f.desc.n_u = 2;
+  f.desc.horizon = horizon;
+  f.desc.cost_scale = 0.5;
+  f.desc.dt = dt;
+  return f;
+}
+
 struct Options {
   int device = 0;
   void* stream = nullptr;  // cudaStream_t; nullptr = legacy default stream

@@ -64,7 +64,8 @@ struct docp_batch {
     std::vector<char> key;
     uint64_t launches = 0;
   };
-  GraphCache graph_fwd, graph_bwd;
+  GraphCache graph_fwd, graph_bwd;  // rollouts
+  GraphCache graph_solve, graph_vjp;  // sqp_solve (<= 4 iterations), backward_vjp
   uint64_t layout_gen = 0;  // bumped whenever a device buffer is reallocated
   // profiling: CUDA events around every launch, per kernel kind, on the batch stream
   bool profiling = false;
@@ -80,6 +81,8 @@ struct docp_batch {
   ~docp_batch() {
     if (graph_fwd.exec) cudaGraphExecDestroy(graph_fwd.exec);
     if (graph_bwd.exec) cudaGraphExecDestroy(graph_bwd.exec);
+    if (graph_solve.exec) cudaGraphExecDestroy(graph_solve.exec);
+    if (graph_vjp.exec) cudaGraphExecDestroy(graph_vjp.exec);
     for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (h_count) cudaFreeHost(h_count);

@@ -170,8 +170,9 @@ int launch_assemble_t(docp_batch* b, const int* list, const int* count, int n_hi
 int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur,
                     bool fast = false) {
   const int nx = b->d.nx, nu = b->d.nu;
-  if (nx == 8 && nu == 4) return launch_assemble_t<8, 4>(b, list, count, n_hint, eps_pd, do_schur, fast);
-  if (nx == 8 && nu == 2) return launch_assemble_t<8, 2>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  const bool shaped = b->prob.family != DOCP_DRIFT;  // the drifting family runs the runtime-shape kernels
+  if (shaped && nx == 8 && nu == 4) return launch_assemble_t<8, 4>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  if (shaped && nx == 8 && nu == 2) return launch_assemble_t<8, 2>(b, list, count, n_hint, eps_pd, do_schur, fast);
   if (nx == 4 && nu == 2) return launch_assemble_t<4, 2>(b, list, count, n_hint, eps_pd, do_schur, fast);
   if (nx == 4 && nu == 1) return launch_assemble_t<4, 1>(b, list, count, n_hint, eps_pd, do_schur, fast);
   if (nx == 16 && nu == 8) return launch_assemble_t<16, 8>(b, list, count, n_hint, eps_pd, do_schur, fast);
@@ -290,7 +291,8 @@ int launch_step(docp_batch* b, const docp_sqp_config& cfg, const int* list, cons
   if (smem + 1024 > static_cast<size_t>(max_optin)) return fail(DOCP_UNSUPPORTED, "line search: horizon too long");
   const int nx = b->d.nx, nu = b->d.nu;
   auto kern = stage ? step_kernel<0, 0, true> : step_kernel<0, 0, false>;
-  if (nx == 8 && nu == 4) kern = stage ? step_kernel<8, 4, true> : step_kernel<8, 4, false>;
+  if (b->prob.family == DOCP_DRIFT) {  // runtime-shape kernel (Family::dynamics' DRIFT branch)
+  } else if (nx == 8 && nu == 4) kern = stage ? step_kernel<8, 4, true> : step_kernel<8, 4, false>;
   else if (nx == 8 && nu == 2) kern = stage ? step_kernel<8, 2, true> : step_kernel<8, 2, false>;
   else if (nx == 4 && nu == 2) kern = step_kernel<4, 2, true>;
   else if (nx == 4 && nu == 1) kern = step_kernel<4, 1, true>;
@@ -314,7 +316,8 @@ int launch_kkt(docp_batch* b, const int* list, const int* count, int n_hint) {
   if (smem + 1024 > static_cast<size_t>(max_optin)) return fail(DOCP_UNSUPPORTED, "kkt_residual: horizon too long");
   auto kern = kkt_kernel<0, 0>;
   const int nx = b->d.nx, nu = b->d.nu;
-  if (nx == 8 && nu == 4) kern = kkt_kernel<8, 4>;
+  if (b->prob.family == DOCP_DRIFT) {  // runtime-shape kernel (Family::dynamics' DRIFT branch)
+  } else if (nx == 8 && nu == 4) kern = kkt_kernel<8, 4>;
   else if (nx == 8 && nu == 2) kern = kkt_kernel<8, 2>;
   else if (nx == 4 && nu == 2) kern = kkt_kernel<4, 2>;
   else if (nx == 4 && nu == 1) kern = kkt_kernel<4, 1>;
@@ -702,11 +705,75 @@ int docp_kkt_residual(docp_batch* b) {
   return launch_kkt(b, b->all_list, b->counts, b->B);
 }
 
+extern "C++" {
+namespace {
+/// Runs `body` (stream work only, no host synchronisation) through a cached
+/// CUDA graph when the batch has its own stream and is not profiling: the
+/// first call with a given key captures and instantiates, later calls replay.
+template <class F>
+int run_graph(docp_batch* b, docp_batch::GraphCache& gc, std::vector<char> key, F&& body) {
+  if (!b->stream || b->profiling || std::getenv("DOCP_NO_GRAPHS")) return body();
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(b->stream, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return body();  // inside an enclosing capture (a rollout graph)
+  const char* gen = reinterpret_cast<const char*>(&b->layout_gen);
+  key.insert(key.end(), gen, gen + sizeof b->layout_gen);
+  if (!(gc.exec && gc.key == key)) {
+    if (gc.exec) {
+      cudaGraphExecDestroy(gc.exec);
+      gc.exec = nullptr;
+    }
+    const uint64_t l0 = g_launches.load();
+    CUDA_TRY(cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = body();
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(b->stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    CUDA_TRY(e);
+    const cudaError_t ei = cudaGraphInstantiate(&gc.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CUDA_TRY(ei);
+    gc.key = key;
+    gc.launches = g_launches.load() - l0;
+    g_launches.fetch_sub(gc.launches);  // counted when the graph runs
+  }
+  CUDA_TRY(cudaGraphLaunch(gc.exec, b->stream));
+  g_launches.fetch_add(gc.launches);
+  return DOCP_OK;
+}
+
+template <class T>
+void key_add(std::vector<char>& k, const T& v) {
+  const char* p = reinterpret_cast<const char*>(&v);
+  k.insert(k.end(), p, p + sizeof v);
+}
+}  // namespace
+}  // extern "C++"
+
+static int sqp_solve_body(docp_batch* b, const docp_sqp_config* cfg);
+
 int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-261
   if (!b) return fail(DOCP_INVALID, "null batch");
   int rc = validate_sqp(cfg);
   if (rc) return rc;
   if ((rc = ensure_hist(b, std::max(1, cfg->max_sqp_iters)))) return rc;
+  // Up to 4 SQP iterations the host never waits on the device (below), so
+  // the whole solve is one cached CUDA graph when the batch has its own
+  // stream: a small-batch call (C1: B = 1, one SQP step) costs one graph
+  // launch instead of ~15 kernel launches.
+  if (cfg->max_sqp_iters <= 4) {
+    std::vector<char> key;
+    key_add(key, *cfg);
+    return run_graph(b, b->graph_solve, key, [&]() { return sqp_solve_body(b, cfg); });
+  }
+  return sqp_solve_body(b, cfg);
+}
+
+static int sqp_solve_body(docp_batch* b, const docp_sqp_config* cfg) {
+  int rc;
   int cur = 0;
   CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, 2 * sizeof(int), b->stream));
   init_solve_kernel<<<grid_for(static_cast<long>(b->B) * 32, 256, b->num_sms * 8), 256, 0, b->stream>>>(b->v, b->list[0], b->counts + 1);
@@ -760,8 +827,16 @@ int docp_sqp_solve(docp_batch* b, const docp_sqp_config* cfg) {  // sqp.hpp:213-
   return DOCP_OK;
 }
 
+static int backward_vjp_body(docp_batch* b, const docp_pcg_config* cfg);
+
 int docp_backward_vjp(docp_batch* b, const docp_pcg_config* cfg) {  // backward.hpp:27-50
   if (!b || !cfg) return fail(DOCP_INVALID, "null argument");
+  std::vector<char> key;
+  key_add(key, *cfg);
+  return run_graph(b, b->graph_vjp, key, [&]() { return backward_vjp_body(b, cfg); });
+}
+
+static int backward_vjp_body(docp_batch* b, const docp_pcg_config* cfg) {
   int rc;
   CUDA_TRY(cudaMemsetAsync(b->counts + 1, 0, sizeof(int), b->stream));
   ok_list_kernel<<<grid_for(b->B, 256, 4096), 256, 0, b->stream>>>(b->v, b->list[0], b->counts + 1);
@@ -790,50 +865,7 @@ int ensure_rollout(docp_batch* b, int H) {
 }
 }  // namespace
 
-extern "C++" {
-namespace {
-/// Runs `body` (stream work only, no host synchronisation) through a cached
-/// CUDA graph when the batch has its own stream and is not profiling: the
-/// first call with a given key captures and instantiates, later calls replay.
-template <class F>
-int run_graph(docp_batch* b, docp_batch::GraphCache& gc, std::vector<char> key, F&& body) {
-  if (!b->stream || b->profiling || std::getenv("DOCP_NO_GRAPHS")) return body();
-  const char* gen = reinterpret_cast<const char*>(&b->layout_gen);
-  key.insert(key.end(), gen, gen + sizeof b->layout_gen);
-  if (!(gc.exec && gc.key == key)) {
-    if (gc.exec) {
-      cudaGraphExecDestroy(gc.exec);
-      gc.exec = nullptr;
-    }
-    const uint64_t l0 = g_launches.load();
-    CUDA_TRY(cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal));
-    const int rc = body();
-    cudaGraph_t graph = nullptr;
-    const cudaError_t e = cudaStreamEndCapture(b->stream, &graph);
-    if (rc) {
-      if (graph) cudaGraphDestroy(graph);
-      return rc;
-    }
-    CUDA_TRY(e);
-    const cudaError_t ei = cudaGraphInstantiate(&gc.exec, graph, 0);
-    cudaGraphDestroy(graph);
-    CUDA_TRY(ei);
-    gc.key = key;
-    gc.launches = g_launches.load() - l0;
-    g_launches.fetch_sub(gc.launches);  // counted when the graph runs
-  }
-  CUDA_TRY(cudaGraphLaunch(gc.exec, b->stream));
-  g_launches.fetch_add(gc.launches);
-  return DOCP_OK;
-}
 
-template <class T>
-void key_add(std::vector<char>& k, const T& v) {
-  const char* p = reinterpret_cast<const char*>(&v);
-  k.insert(k.end(), p, p + sizeof v);
-}
-}  // namespace
-}  // extern "C++"
 
 int docp_rollout(docp_batch* b, const docp_sqp_config* cfg, const double* x_init, int32_t x_init_on_device,
                  int32_t H) {

@@ -27,6 +27,20 @@ __device__ inline double diag_cost_value(double scale, const double* w, const do
 __device__ inline double diag_cost_grad(double scale, double w, double v) { return ((2.0 * scale) * w) * v; }
 __device__ inline double diag_cost_hess(double scale, double w) { return (2.0 * scale) * w; }
 
+/// The drifting family's residual and Jacobians, out of line: its dual-number
+/// evaluation needs a large stack frame that must not inflate the kernels
+/// (step, KKT, linearize) for the families that never call it.
+__device__ __noinline__ void drift_dynamics(const double* th, double dt, const double* xn, const double* x,
+                                            const double* u, double* res, double* jx, double* ju) {
+  double xn_[docp_drift::NX], jxx[docp_drift::NX * docp_drift::NX], juu[docp_drift::NX * docp_drift::NU];
+  docp_drift::step(th, dt, x, u, xn_, jx ? jxx : nullptr, ju ? juu : nullptr);
+  for (int i = 0; i < docp_drift::NX; ++i) res[i] = xn[i] - xn_[i];
+  if (jx)
+    for (int k = 0; k < docp_drift::NX * docp_drift::NX; ++k) jx[k] = -jxx[k];
+  if (ju)
+    for (int k = 0; k < docp_drift::NX * docp_drift::NU; ++k) ju[k] = -juu[k];
+}
+
 struct Family {
   int kind;
   double scale;
@@ -55,7 +69,11 @@ struct Family {
   /// Dynamics residual f = x+ - phi(x, u) and its Jacobians (jac_x_next = I).
   /// res[nx]; jx[nx*nx], ju[nx*nu] column-major (may be null). NX, NU > 0
   /// fix the sizes at compile time (same arithmetic, unrolled).
-  template <int NX = 0, int NU = 0>
+  /// DRIFT: whether the drifting family's branch is compiled in. Only the
+  /// runtime-shape kernels (NX = 0) carry it; the launchers route DOCP_DRIFT
+  /// to them, so the compile-time-shape kernels of the other families keep
+  /// their register budgets (the model's dual-number Jacobians need ~255).
+  template <int NX = 0, int NU = 0, bool DRIFT = (NX == 0)>
   __device__ void dynamics(const Dims& d, const double* th, const double* xn, const double* x, const double* u,
                            double* res, double* jx, double* ju) const {
     const int nx = NX ? NX : d.nx, nu = NU ? NU : d.nu;
@@ -79,15 +97,11 @@ struct Family {
         for (int k = 0; k < nx * nu; ++k) ju[k] = -b[k];
       return;
     }
-    if (kind == DOCP_DRIFT) {  // make_explicit_dynamics(docp_drift::step): the shared model definition
-      double xn_[docp_drift::NX], jxx[docp_drift::NX * docp_drift::NX], juu[docp_drift::NX * docp_drift::NU];
-      docp_drift::step(th, dt, x, u, xn_, jx ? jxx : nullptr, ju ? juu : nullptr);
-      for (int i = 0; i < docp_drift::NX; ++i) res[i] = xn[i] - xn_[i];
-      if (jx)
-        for (int k = 0; k < docp_drift::NX * docp_drift::NX; ++k) jx[k] = -jxx[k];
-      if (ju)
-        for (int k = 0; k < docp_drift::NX * docp_drift::NU; ++k) ju[k] = -juu[k];
-      return;
+    if constexpr (DRIFT) {
+      if (kind == DOCP_DRIFT) {  // make_explicit_dynamics(docp_drift::step): the shared model definition
+        drift_dynamics(th, dt, xn, x, u, res, jx, ju);
+        return;
+      }
     }
     if (kind == DOCP_ATTITUDE) {  // make_explicit_dynamics(attitude_step), attitude.hpp:16-42
       const double* in = th + 9;   // AttitudeParams::inertia (THETA tail)

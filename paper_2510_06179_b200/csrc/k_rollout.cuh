@@ -26,7 +26,7 @@ __device__ inline void env_step(const Dims& d, const Family& fam, const double* 
                                 double* xn) {
   double zero[kMaxNx], res[kMaxNx];
   for (int i = 0; i < d.nx; ++i) zero[i] = 0.0;
-  fam.dynamics(d, th, zero, x, u, res, nullptr, nullptr);
+  fam.dynamics<0, 0, false>(d, th, zero, x, u, res, nullptr, nullptr);
   for (int i = 0; i < d.nx; ++i) xn[i] = -res[i];
 }
 
@@ -152,7 +152,7 @@ __global__ void rollout_back_pre_kernel(View v, RolloutRec rr, int t, int* __res
     if (lane == 0) {
       // step_vjp: the step's Jacobians (dphi/dx, dphi/du) = -(jac_x, jac_u) of the residual
       double jx[kMaxNx * kMaxNx], ju[kMaxNx * kMaxNu], res[kMaxNx];
-      fam.dynamics(d, th, xn, x, u, res, jx, ju);
+      fam.dynamics<0, 0, false>(d, th, xn, x, u, res, jx, ju);
       double* xbar = rr.xbar + static_cast<long>(p) * nx;
       double* ex = rr.ex + static_cast<long>(p) * nx;
       const double rx = fam.kind == DOCP_ATTITUDE ? -0.2 : -2.0;  // reward_grad (train.hpp:208-211, 254-257)

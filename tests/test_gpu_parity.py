@@ -737,3 +737,39 @@ def test_aq_blocks_kept_across_sqp_iterations(D, mode, monkeypatch):
     full_run = run()
     for a, c in zip(kept_run, full_run):
         assert np.array_equal(a, c)
+
+
+def test_solve_and_backward_graphs_replay_bitwise(D):
+    """With a batch stream, sqp_solve (<= 4 SQP iterations) and backward_vjp run
+    as cached CUDA graphs (the C1 small-batch path): the first call captures,
+    later calls replay. Replays on new inputs equal the direct launches bit
+    for bit."""
+    import torch
+    nx, nu, T, B = 4, 2, 20, 3
+    prob = D.affine_quadratic(nx, nu, T)
+    nz, nl = D.sizes(prob)
+    cfg = D.one_shot_config(mode="parity")
+    outs = {}
+    for graphs in (True, False):
+        b = D.Batch(prob, B)
+        if graphs:
+            stream = torch.cuda.Stream()
+            b.set_stream(stream.cuda_stream)
+        res = []
+        for seed in (0, 1, 2):  # capture, then two replays on different data
+            th = D.generate_affine_quadratic(nx, nu, seed, B)
+            b.upload(D._lib.F_THETA, th)
+            b.upload(D._lib.F_Z, np.zeros((B, nz)))
+            b.upload(D._lib.F_LAMBDA, np.zeros((B, nl)))
+            l0 = D.kernel_launches()
+            b.sqp_solve(cfg)
+            z = b.download(D._lib.F_Z)
+            b.upload(D._lib.F_LOSS_GRAD_Z, 2.0 * z)
+            b.upload(D._lib.F_LAMBDA_TILDE, np.zeros((B, nl)))
+            b.backward_vjp(cfg.pcg)
+            b.sync()
+            res.append((z.copy(), b.download(D._lib.F_GRAD_THETA).copy(), D.kernel_launches() - l0))
+        outs[graphs] = res
+    for (zg, gg, ng), (zd, gd, nd) in zip(outs[True], outs[False]):
+        assert np.array_equal(zg, zd) and np.array_equal(gg, gd)
+        assert ng == nd  # launches inside a replayed graph are still counted

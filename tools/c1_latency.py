@@ -60,9 +60,14 @@ def main():
             return o.backward(th, 2.0 * s.z, np.zeros(nl))[0]
         ref_grad = cpu()
         out["reference_cpu_us"], out["reference_cpu_p90_us"] = median_us(cpu, args.reps)
-    for mode in ("parity", "fast"):
+    import torch
+    for mode, graphs in (("parity", True), ("fast", True), ("parity", False), ("fast", False)):
         cfg = D.one_shot_config(mode=mode)
         b = D.Batch(prob, 1)
+        if graphs:  # a batch stream: sqp_solve (one SQP step) and backward_vjp replay cached CUDA graphs
+            stream = torch.cuda.Stream()
+            b.set_stream(stream.cuda_stream)
+        tag = mode if graphs else mode + "_nograph"
         z0, l0 = np.zeros((1, nz)), np.zeros((1, nl))
 
         def gpu():
@@ -78,11 +83,11 @@ def main():
         g = gpu()
         if ref_grad is not None:
             rel = float(np.linalg.norm(g - ref_grad) / np.linalg.norm(ref_grad))
-            out[f"gpu_{mode}_rel_err_vs_reference"] = rel
+            out[f"gpu_{tag}_rel_err_vs_reference"] = rel
         l0_ = D.kernel_launches()
         gpu()
-        out[f"gpu_{mode}_kernels_per_call"] = D.kernel_launches() - l0_
-        out[f"gpu_{mode}_us"], out[f"gpu_{mode}_p90_us"] = median_us(gpu, args.reps)
+        out[f"gpu_{tag}_kernels_per_call"] = D.kernel_launches() - l0_
+        out[f"gpu_{tag}_us"], out[f"gpu_{tag}_p90_us"] = median_us(gpu, args.reps)
     print(json.dumps(out))
     if args.json:
         with open(args.json, "w") as fh:
