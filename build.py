@@ -27,7 +27,7 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-UNITS = ["docp_cuda.cu", "pcg_nx8.cu", "pcg_nx4.cu", "pcg_nx16.cu", "pcg_nxrt.cu", "generators.cpp"]
+UNITS = ["docp_cuda.cu", "pcg_nx8.cu", "pcg_nx4.cu", "pcg_nx16.cu", "pcg_nxrt.cu", "pcg_nxct.cu", "generators.cpp"]
 
 
 def build_cuda(force=False, verbose=False, lib=None, extra_flags=()):

@@ -150,5 +150,7 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8);
 int launch_pcg_fp32_nx8(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
                         int max_iters);
 DOCP_PCG_LAUNCHER(launch_pcg_nxrt);
+DOCP_PCG_LAUNCHER(launch_pcg_nx6);
+DOCP_PCG_LAUNCHER(launch_pcg_nx9);
 
 }  // namespace docp_host

@@ -268,6 +268,8 @@ int launch_pcg(docp_batch* b, const docp_pcg_config& cfg, const int* list, const
     case 4: return launch_pcg_nx4(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
     case 8: return launch_pcg_nx8(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
     case 16: return launch_pcg_nx16(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+    case 6: return launch_pcg_nx6(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
+    case 9: return launch_pcg_nx9(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
     default: return launch_pcg_nxrt(b, pl, par, list, count, n_hint, sol, cfg.epsilon, cfg.max_iters);
   }
 }
@@ -1099,12 +1101,12 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
                            d.nx == 8 ? "pcg_kernel_h8s; uploaded systems pcg_kernel_h8r" : fk);
   else if (cl > 1) snprintf(fast, sizeof fast, "%s(cluster%d,resident)", fk, cl);
   else snprintf(fast, sizeof fast, "%s", d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
-                                                   : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>");
+                                                   : d.nx == 4 ? "pcg_kernel<4>" : (d.nx == 6 || d.nx == 9) ? "pcg_kernel<NX=6|9>" : "pcg_kernel<runtime>");
   const int p8 = d.nx == 8 ? h8p_variant_for(d, dev) : 0;
   const char* parity = p8 == 1   ? "pcg_kernel_h8p<prefetch>; uploaded systems pcg_kernel_h8"
                        : p8 == 2 ? "pcg_kernel_h8p<no-prefetch>; uploaded systems pcg_kernel_h8"
                        : d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
-                                   : d.nx == 4 ? "pcg_kernel<4>" : "pcg_kernel<runtime>";
+                                   : d.nx == 4 ? "pcg_kernel<4>" : (d.nx == 6 || d.nx == 9) ? "pcg_kernel<NX=6|9>" : "pcg_kernel<runtime>";
   return snprintf(buf, cap, "nx=%d layout=%s record=%ld B parity=%s(%s) fast=%s", d.nx,
                   d.nx == 8 ? "swizzle8" : d.nx == 4 ? "swizzle4" : "colmajor", d.blk_stride * 8, parity,
                   res ? "resident" : "streaming", fast);

@@ -276,7 +276,8 @@ def _oracle_solve_and_grad(pprob, th, z0, lam0, cfg_port, lg, lt0):
 
 @pytest.mark.parametrize("mode", ["parity", "fast"])
 @pytest.mark.parametrize("nx,nu,T,seed,max_it", [(4, 2, 20, 11, 20), (8, 4, 30, 12, 20), (8, 4, 100, 13, 5),
-                                                 (8, 4, 127, 16, 5), (3, 2, 4, 14, 20), (16, 8, 30, 15, 20)])
+                                                 (8, 4, 127, 16, 5), (3, 2, 4, 14, 20), (16, 8, 30, 15, 20),
+                                                 (9, 2, 100, 17, 5)])
 def test_sqp_backward_affine_quadratic(D, mode, nx, nu, T, seed, max_it):
     B = 4
     th = aq_thetas(nx, nu, T, seed, B)

@@ -47,17 +47,18 @@ def hbm_peak():
 
 
 NU = 4
+NX = 8
 
 
 def run(T, B, reps, pool_cache, chunk=65536):
-    prob = D.affine_quadratic(8, NU, T)
+    prob = D.affine_quadratic(NX, NU, T)
     nz, nl = D.sizes(prob)
     if T not in pool_cache:
         pool_cache.clear()
-        pool_cache[T] = D.generate_affine_quadratic(8, NU, 0, min(B, POOL), convex=CONVEX)
+        pool_cache[T] = D.generate_affine_quadratic(NX, NU, 0, min(B, POOL), convex=CONVEX)
     pool = pool_cache[T]
     if len(pool) < min(B, POOL):
-        pool = pool_cache[T] = D.generate_affine_quadratic(8, NU, 0, min(B, POOL), convex=CONVEX)
+        pool = pool_cache[T] = D.generate_affine_quadratic(NX, NU, 0, min(B, POOL), convex=CONVEX)
     th = np.resize(pool, (B, pool.shape[1])) if B > len(pool) else pool[:B]
     C = min(B, chunk)
     assert B % C == 0, "the chunk size must divide the batch"
@@ -97,7 +98,7 @@ def run(T, B, reps, pool_cache, chunk=65536):
             "pcg_iters_per_solve": prof["pcg_iterations"] / max(1, prof["pcg_solves"]),
             "pcg_share": pcg_ms / total_kernel if total_kernel else None, "pcg_algorithmic_GBps": gbs,
             "pcg_frac_hbm": gbs / hbm_peak(), "pcg_kernel": D.describe(prob), "failed_instances": errs,
-            "block_record_MB": B * 16 * 64 * (2 * T + 1) / 1e6, "chunks": B // C}
+            "block_record_MB": B * 16 * NX * NX * (2 * T + 1) / 1e6, "chunks": B // C}
 
 
 def main():
@@ -108,10 +109,11 @@ def main():
     ap.add_argument("--md", default=None)
     ap.add_argument("--chunk", type=int, default=65536)
     ap.add_argument("--nu", type=int, default=4)
+    ap.add_argument("--nx", type=int, default=8)
     ap.add_argument("--convex", action="store_true", help="random_convex_instance draws (domain-randomised weights)")
     a = ap.parse_args()
-    global NU, CONVEX
-    NU, CONVEX = a.nu, a.convex
+    global NU, NX, CONVEX
+    NU, NX, CONVEX = a.nu, a.nx, a.convex
     rows = []
     cache = {}
     for T in [int(x) for x in a.T.split(",")]:
@@ -123,7 +125,7 @@ def main():
     if a.md:
         with open(a.md, "w") as fh:
             fh.write("# Sweep — solve + gradient on one B200 (FAST, cold caches, median of %d)\n\n" % a.reps)
-            fh.write(f"Workload: `{'random_convex_instance' if CONVEX else 'random_linear_instance'}(8, {NU}, T)` "
+            fh.write(f"Workload: `{'random_convex_instance' if CONVEX else 'random_linear_instance'}({NX}, {NU}, T)` "
                      "draws, `sqp_solve` (5 SQP iterations max, "
                      "eps 1e-12) + `backward_vjp` per problem. PCG GB/s = algorithmic bytes "
                      "(SURVEY.md §8(d)) / PCG kernel time; HBM peak %.1f GB/s (MEASURED_PEAKS.json).\n\n" % hbm_peak())
