@@ -138,13 +138,13 @@ __global__ void reset_status_kernel(View v) {
 }
 
 // ---------------------------------------------------------------- launch helpers
-template <int NX, int NU, int TH>
+template <int NX, int NU, int TH, bool DR = false>
 int launch_assemble_th(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur,
                        bool fast) {
   constexpr int NG = TH / NX;
   // NG group buffers + the two-block P_t hand-off between rounds
   const size_t smem = (static_cast<size_t>(NG) * AsmLayout<NX, NU>::GBUF + 2 * AsmLayout<NX, NU>::P2) * sizeof(double);
-  auto kern = fast ? assemble_kernel_t<NX, NU, TH, true> : assemble_kernel_t<NX, NU, TH, false>;
+  auto kern = fast ? assemble_kernel_t<NX, NU, TH, true, DR> : assemble_kernel_t<NX, NU, TH, false, DR>;
   if (do_schur) b->sym_blocks = true;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
@@ -158,10 +158,10 @@ int launch_assemble_th(docp_batch* b, const int* list, const int* count, int n_h
 
 /// 128 threads: 16 groups of 8 lanes (n_x = 8). A 160-thread variant (whole
 /// rounds at T = 100) measured 3% slower: occupancy fell from 16 to 15 warps/SM.
-template <int NX, int NU>
+template <int NX, int NU, bool DR = false>
 int launch_assemble_t(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur,
                       bool fast) {
-  return launch_assemble_th<NX, NU, kAsmGroupThreads>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  return launch_assemble_th<NX, NU, kAsmGroupThreads, DR>(b, list, count, n_hint, eps_pd, do_schur, fast);
 }
 
 /// K1. fast (PCG mode FAST): reciprocal / fma arithmetic in the compile-time
@@ -170,8 +170,14 @@ int launch_assemble_t(docp_batch* b, const int* list, const int* count, int n_hi
 int launch_assemble(docp_batch* b, const int* list, const int* count, int n_hint, double eps_pd, int do_schur,
                     bool fast = false) {
   const int nx = b->d.nx, nu = b->d.nu;
-  const bool shaped = b->prob.family != DOCP_DRIFT;  // the drifting family runs the runtime-shape kernels
-  if (shaped && nx == 8 && nu == 4) return launch_assemble_t<8, 4>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  // the drifting family runs its own instantiation (the model's dual-number
+  // Jacobians need ~255 registers; the other families' kernels leave it out)
+  if (b->prob.family == DOCP_DRIFT) {
+    if (nx == 8 && nu == 2) return launch_assemble_t<8, 2, true>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  } else if (nx == 8 && nu == 4) {
+    return launch_assemble_t<8, 4>(b, list, count, n_hint, eps_pd, do_schur, fast);
+  }
+  const bool shaped = b->prob.family != DOCP_DRIFT;
   if (shaped && nx == 8 && nu == 2) return launch_assemble_t<8, 2>(b, list, count, n_hint, eps_pd, do_schur, fast);
   if (nx == 4 && nu == 2) return launch_assemble_t<4, 2>(b, list, count, n_hint, eps_pd, do_schur, fast);
   if (nx == 4 && nu == 1) return launch_assemble_t<4, 1>(b, list, count, n_hint, eps_pd, do_schur, fast);
@@ -293,7 +299,8 @@ int launch_step(docp_batch* b, const docp_sqp_config& cfg, const int* list, cons
   if (smem + 1024 > static_cast<size_t>(max_optin)) return fail(DOCP_UNSUPPORTED, "line search: horizon too long");
   const int nx = b->d.nx, nu = b->d.nu;
   auto kern = stage ? step_kernel<0, 0, true> : step_kernel<0, 0, false>;
-  if (b->prob.family == DOCP_DRIFT) {  // runtime-shape kernel (Family::dynamics' DRIFT branch)
+  if (b->prob.family == DOCP_DRIFT) {  // the drifting family's instantiation (Family::dynamics' DRIFT branch)
+    if (nx == 8 && nu == 2) kern = stage ? step_kernel<8, 2, true, true> : step_kernel<8, 2, false, true>;
   } else if (nx == 8 && nu == 4) kern = stage ? step_kernel<8, 4, true> : step_kernel<8, 4, false>;
   else if (nx == 8 && nu == 2) kern = stage ? step_kernel<8, 2, true> : step_kernel<8, 2, false>;
   else if (nx == 4 && nu == 2) kern = step_kernel<4, 2, true>;
@@ -318,7 +325,8 @@ int launch_kkt(docp_batch* b, const int* list, const int* count, int n_hint) {
   if (smem + 1024 > static_cast<size_t>(max_optin)) return fail(DOCP_UNSUPPORTED, "kkt_residual: horizon too long");
   auto kern = kkt_kernel<0, 0>;
   const int nx = b->d.nx, nu = b->d.nu;
-  if (b->prob.family == DOCP_DRIFT) {  // runtime-shape kernel (Family::dynamics' DRIFT branch)
+  if (b->prob.family == DOCP_DRIFT) {  // the drifting family's instantiation (Family::dynamics' DRIFT branch)
+    if (nx == 8 && nu == 2) kern = kkt_kernel<8, 2, true>;
   } else if (nx == 8 && nu == 4) kern = kkt_kernel<8, 4>;
   else if (nx == 8 && nu == 2) kern = kkt_kernel<8, 2>;
   else if (nx == 4 && nu == 2) kern = kkt_kernel<4, 2>;

@@ -185,7 +185,7 @@ __device__ void linearize_aq_rows(const View& v, int p, double eps_pd, const Fam
 /// given, is shared memory for nz + nth doubles: z and theta are first
 /// copied there with coalesced loads, so the per-stage tasks read on-chip
 /// copies instead of issuing dependent global loads.
-template <int NX = 0, int NU = 0>
+template <int NX = 0, int NU = 0, bool DR = (NX == 0)>
 __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schur, AsmShared& sh,
                                 double* stage = nullptr) {
   const Dims d = v.d;
@@ -278,7 +278,7 @@ __device__ bool phase_linearize(const View& v, int p, double eps_pd, int do_schu
       const bool write_jac = tv || t == 0;
       double* jx = v.A + a_off(d, p, t);
       double* ju = v.Bm + b_off(d, p, t);
-      fam.dynamics<NX, NU>(d, th, xn, x, u, res, write_jac ? jx : nullptr, write_jac ? ju : nullptr);
+      fam.dynamics<NX, NU, DR>(d, th, xn, x, u, res, write_jac ? jx : nullptr, write_jac ? ju : nullptr);
       bool dfin = true;
       for (int i = 0; i < nx; ++i) dfin = dfin && isfinite(res[i]);
       if (write_jac) {
@@ -549,7 +549,9 @@ struct AsmLayout {
 /// takes 1/l_kk = rsqrt(pivot) and keeps it on the factor's diagonal for the
 /// triangular solves — and fma accumulation. FAST = false is the
 /// reference's arithmetic bit for bit.
-template <int NX, int NU, int TH, bool FAST>
+/// DR: the instantiation for the drifting family (Family::dynamics' DRIFT
+/// branch compiled in; the other families' instantiations leave it out).
+template <int NX, int NU, int TH, bool FAST, bool DR = false>
 __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assemble_kernel_t(View v, const int* __restrict__ work,
                                                                       const int* __restrict__ n_work, double eps_pd,
                                                                       int do_schur) {
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
     // z / theta staged in the group buffers (free until phase B) when they fit
-    if (!phase_linearize<NX, NU>(v, p, eps_pd, do_schur, sh, stage_in ? sm_asm : nullptr)) {
+    if (!phase_linearize<NX, NU, DR>(v, p, eps_pd, do_schur, sh, stage_in ? sm_asm : nullptr)) {
       __syncthreads();
       continue;
     }

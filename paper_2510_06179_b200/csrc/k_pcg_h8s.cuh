@@ -94,7 +94,7 @@ __host__ __device__ inline long h8s_smem_doubles(const Dims& d) {
 /// are loaded one after the other into the same region. pcg_kernel_h8s_wide
 /// (below) extends that to T <= 191.
 #ifdef DOCP_H8S_CLOCK
-__device__ unsigned long long g_h8s_clk[12];
+__device__ unsigned long long g_h8s_clk[16];
 #define H8S_CLK(k)                        \
   if (tid == 0) {                         \
     const long long t_ = clock64();       \
@@ -128,7 +128,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int nwk = *n_work;
 #ifdef DOCP_H8S_CLOCK
-  long long clk[12] = {0}, t_last = clock64();
+  long long clk[16] = {0}, t_last = clock64();
 #endif
 
   constexpr int NWS = MAXT <= 256 ? 8 : 16;  // warp slots per dot
@@ -355,9 +355,12 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       double xf[8], own[4], hand[4], low[4], up[4], xn[4];
       gather(xr, xf);
       put(vbuf, my0, my1, xr);
+      H8S_CLK(12);
       h8s::sym_times(sd, xf, xr, h, own);
+      H8S_CLK(13);
       rows_times(so, xf, hand);  // L_i x_i
       put(xbuf, pv0, pv1, hand);  // slot i (see pp0 above)
+      H8S_CLK(14);
       partial(a, b, slot);
       H8S_CLK(0);
       __syncthreads();
@@ -487,7 +490,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   }
 #ifdef DOCP_H8S_CLOCK
   if (tid == 0)
-    for (int k = 0; k < 12; ++k) atomicAdd(&g_h8s_clk[k], static_cast<unsigned long long>(clk[k]));
+    for (int k = 0; k < 16; ++k) atomicAdd(&g_h8s_clk[k], static_cast<unsigned long long>(clk[k]));
 #endif
 }
 

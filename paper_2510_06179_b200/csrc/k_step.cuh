@@ -34,7 +34,7 @@ struct StepCfg {
 /// t -> 2T+1+t, initial-condition |x_0 - x_s|_1 -> 3T+1. zo, zq, th are the
 /// problem's shared-memory copies; a non-finite cost value lowers *first_bad
 /// to its slot (merit_parts throws at the first one in slot order).
-template <int NX, int NU>
+template <int NX, int NU, bool DR = (NX == 0)>
 __device__ inline void merit_task(const Dims& d, const Family& fam, const double* th, const double* zo,
                                   const double* zq, int P, double alpha, bool trial, int task, double* slots,
                                   int* first_bad) {
@@ -61,7 +61,7 @@ __device__ inline void merit_task(const Dims& d, const Family& fam, const double
     const double val = diag_cost_value<NU>(fam.scale, fam.w_u(d, th), b, nu);
     slots[T + 1 + t] = val;
     if (!isfinite(val)) atomicMin(first_bad, T + 1 + t);
-    fam.dynamics<NX, NU>(d, th, c, a, b, res, nullptr, nullptr);
+    fam.dynamics<NX, NU, DR>(d, th, c, a, b, res, nullptr, nullptr);
     double s = fabs(res[0]);
 #pragma unroll
     for (int i = 1; i < nx; ++i) s = s + fabs(res[i]);
@@ -110,7 +110,7 @@ __host__ __device__ inline long step_smem_doubles(const Dims& d, int n_alpha, bo
 /// z_qp and theta are staged in shared memory, the stage terms of every
 /// version are evaluated in parallel, and each sum is folded by one thread
 /// in the reference's order. NX, NU > 0 fix the block sizes at compile time.
-template <int NX, int NU, bool STAGE = true>
+template <int NX, int NU, bool STAGE = true, bool DR = (NX == 0)>
 __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* __restrict__ work,
                                                            const int* __restrict__ n_work, StepCfg cfg) {
   extern __shared__ double sm_step[];
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
     for (int task = tid; task < nver * (2 * T + 2); task += blockDim.x) {
       const int ver = task / (2 * T + 2);
       const int tt = task - ver * (2 * T + 2);
-      merit_task<NX, NU>(d, fam, sth, szo, szq, P, ver == 0 ? 0.0 : cfg.alphas[ver - 1], ver > 0, tt,
+      merit_task<NX, NU, DR>(d, fam, sth, szo, szq, P, ver == 0 ? 0.0 : cfg.alphas[ver - 1], ver > 0, tt,
                          slots + static_cast<long>(ver) * nslot, &s_bad[ver]);
     }
     __syncthreads();
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(View v, const int* _
 /// problem with z, lambda and theta staged in shared memory, one thread per
 /// stage. NX, NU > 0 fix the block sizes at compile time.
 constexpr int kKktThreads = 128;
-template <int NX, int NU>
+template <int NX, int NU, bool DR = (NX == 0)>
 __global__ void __launch_bounds__(kKktThreads, 4) kkt_kernel(View v, const int* __restrict__ work,
                                                         const int* __restrict__ n_work) {
   extern __shared__ double sm_kkt[];
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kKktThreads, 4) kkt_kernel(View v, const int* 
       double jx[AX * AX], ju[AX * AU], res[AX];
       const double* wx = fam.w_x(d, th);
       // grad_l for x_t: cost grad, + lambda_t (A+_{t-1}' lambda_t, or lambda_0 last), + A_t' lambda_{t+1}
-      if (t < T) fam.dynamics<NX, NU>(d, th, z + (t + 1) * P, z + t * P, z + t * P + nx, res, jx, ju);
+      if (t < T) fam.dynamics<NX, NU, DR>(d, th, z + (t + 1) * P, z + t * P, z + t * P + nx, res, jx, ju);
 #pragma unroll
       for (int i = 0; i < AX; ++i) {
         if (i >= nx) break;

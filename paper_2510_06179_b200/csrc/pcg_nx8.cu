@@ -271,8 +271,8 @@ extern "C" int docp_h8p_clock(unsigned long long* out) {
 #ifdef DOCP_H8S_CLOCK
 /// A/B builds only: cycles of pcg_kernel_h8s's thread 0 per phase, summed over launches (then reset).
 extern "C" int docp_h8s_clock(unsigned long long* out) {
-  if (cudaMemcpyFromSymbol(out, docp_dev::g_h8s_clk, 12 * sizeof(unsigned long long)) != cudaSuccess) return 1;
-  static const unsigned long long zero[12] = {0};
+  if (cudaMemcpyFromSymbol(out, docp_dev::g_h8s_clk, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  static const unsigned long long zero[16] = {0};
   return cudaMemcpyToSymbol(docp_dev::g_h8s_clk, zero, sizeof zero) != cudaSuccess;
 }
 #endif

@@ -43,16 +43,17 @@ for fn in ("docp_h8p_clock", "docp_h8s_clock"):  # A/B builds with -DDOCP_H8P_CL
     if not hasattr(L.lib(), fn):
         continue
     import ctypes as C
-    buf = (C.c_ulonglong * 12)()
+    buf = (C.c_ulonglong * 16)()
     getattr(L.lib(), fn)(buf)
     if not sum(buf):
         continue
     its = a.iters * a.reps * -(-a.B // 148)  # iterations seen by CTA 0's thread 0 (approx.)
     names = (["S phase1", "barrier", "S phase2", "P phase2", "P phase1", "-", "dot partial", "dot barrier",
               "chain+bcast", "alpha/beta/updates", "loop exit", "setup"] if fn == "docp_h8p_clock" else
-             ["S phase1 + eta partial", "barriers", "S phase2", "P phase1", "P phase 1b (U)", "P phase2",
-              "dot partial", "dot barrier", "dot total", "alpha + updates", "beta + updates", "setup"])
+             ["S phase1: eta partial", "barriers", "S phase2", "P phase1", "P phase 1b (U)", "P phase2",
+              "dot partial", "dot barrier", "dot total", "alpha + updates", "beta + updates", "setup",
+              "S phase1: gather + put", "S phase1: sym_times", "S phase1: L x + put", "-"])
     tot = sum(buf)
-    for k in range(12):
-        if buf[k]:
+    for k in range(len(buf)):
+        if buf[k] and k < len(names):
             print(f"  {names[k]:24s} {buf[k] / 148 / its:8.0f} cycles/iter  {100 * buf[k] / tot:5.1f}%")
