@@ -181,13 +181,17 @@ __device__ unsigned long long g_h8p_clk[16];
 #define H8P_CLK(k)
 #endif
 
-template <int MAXT, bool PREFETCH>
+/// CW: a CTA of 8 warps whose last warp holds no block rows (T <= 111) folds
+/// the block dots there (one extra barrier per dot, the fold from registers).
+constexpr int CW_WARP = 7;
+template <int MAXT, bool PREFETCH, bool CW = false>
 __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, const int* __restrict__ n_work,
                                          int* __restrict__ counter, double* __restrict__ sol_all, double epsilon,
                                          int max_iters_cfg) {
   extern __shared__ __align__(128) double sm_pcg[];
   __shared__ __align__(8) uint64_t s_bar[2];  // [0]: staged -S blocks, [1]: Phi^-1 blocks
   __shared__ int s_next, s_pidx;
+  __shared__ double s_dot;
   const Dims d = v.d;
   const int nl = d.nl, nb = d.nb;
   const int tid = threadIdx.x;
@@ -197,7 +201,7 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
   const bool act = i < nb;
   const bool has_next = act && i + 1 < nb;
   const bool has_prev = i > 0;
-  const int lane = tid & 31;
+  const int lane = tid & 31, warp = tid >> 5;
   const int nwk = *n_work;
 #ifdef DOCP_H8P_CLOCK
   long long clk[12] = {0}, t_last = clock64();
@@ -299,6 +303,40 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
     H8P_CLK(6);
     __syncthreads();
     H8P_CLK(7);
+    if constexpr (CW) {
+      // warp 7 holds no block rows: its lane 0 folds the block dots with all
+      // of them in flight at once (its registers are free), the others wait
+      if (warp == CW_WARP) {
+        if (lane == 0) {
+          const int nfull = nb & ~15;
+          double tail[15];
+#pragma unroll
+          for (int t = 0; t < 15; ++t) tail[t] = nfull + t < nb ? seg[nfull + t] : 0.0;
+          double cur[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) cur[t] = nfull > 0 ? seg[t] : 0.0;
+          double acc = 0.0;
+          for (int k = 0; k < nfull; k += 16) {
+            const int kn = k + 16 < nfull ? k + 16 : k;
+            double nxt[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) nxt[t] = seg[kn + t];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) acc = acc + cur[t];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) cur[t] = nxt[t];
+          }
+#pragma unroll
+          for (int t = 0; t < 15; ++t)
+            if (nfull + t < nb) acc = acc + tail[t];
+          s_dot = acc;
+        }
+      }
+      __syncthreads();
+      const double tot = s_dot;
+      H8P_CLK(8);
+      return tot;
+    }
     double acc = 0.0;
     if (lane == 0) {
       // software-pipelined: the next 8 block dots are loaded while the current
@@ -429,33 +467,18 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
       finish(own, low, up, out);
     };
     // y = Phi^-1 x: U_i read from shared memory (W = U_i')
+    // y = Phi^-1 x: the diagonal rows and U_i from shared memory (W = U_i'),
+    // U_i's two quarters read ONCE per product: phase 1 exchanges x, then
+    // both the hand-over (W's rows) and the super term (W's columns) are
+    // folded from the same registers, and a second barrier hands the
+    // hand-over on (each thread's quarters serve the hand-over's first and
+    // second halves as f, g, and the super term's as f, g for h = 0 and as
+    // g, f for h = 1).
     auto matvec_p = [&](const double* xr, double* out) {
-      double xf[8], own[4], hf[4], hs[4], low[4], up[4], xn[8];
+      double xf[8], own[4], hs[4], low[4], up[4];
       gather(xr, xf);
       put(vbuf, my0, my1, xr);
-      {
-        double f[4][4], g[4][4];  // f[q][c] = U(c, 4h + q), g[q][c] = U(4 + c, 4(1-h) + q)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const double2 a = *reinterpret_cast<const double2*>(PuI + (bf ^ (8 * q + 2 * j)));
-            f[q][2 * j] = a.x, f[q][2 * j + 1] = a.y;
-            const double2 b = *reinterpret_cast<const double2*>(PuI + (bg ^ (8 * q + 2 * j)));
-            g[q][2 * j] = b.x, g[q][2 * j + 1] = b.y;
-          }
-        h8p::first_halves(f, xf, hf);
-        // second halves after the partner's first halves (4 rounds)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          double acc = __shfl_xor_sync(0xffffffffu, hf[q], 1);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc = acc + g[q][c] * xf[4 + c];
-          hs[q] = acc;
-        }
-      }
-      // own rows of Phi^-1_ii x from shared memory (the block stays there for
-      // the whole solve): row 4h + q = column 4h + q (symmetric), a full fold
+      // own rows of Phi^-1_ii x (row 4h + q = column 4h + q, symmetric): full folds
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         double col[8];
@@ -469,26 +492,38 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
         for (int c = 1; c < 8; ++c) acc = acc + col[c] * xf[c];
         own[q] = acc;
       }
-      put(xbuf, ho0, ho1, hs);
       H8P_CLK(4);
-      __syncthreads();
+      __syncthreads();  // x_{i+1} published
       H8P_CLK(1);
-      get(vbuf, nf0, nf1, xn);
-      get(vbuf, nf2, nf3, xn + 4);
       {
-        // up_r = sum_c U(r, c) x_{i+1}[c]: c1[c][q] = U(4h + q, c), c2[c][q] = U(4(1-h) + q, 4 + c)
-        double c1[4][4], c2[4][4];
+        double f[4][4], g[4][4];  // f[q][c] = U(c, 4h + q), g[q][c] = U(4 + c, 4(1-h) + q)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            const double2 a = *reinterpret_cast<const double2*>(PuI + (b1 ^ (8 * c + 2 * j)));
-            c1[c][2 * j] = a.x, c1[c][2 * j + 1] = a.y;
-            const double2 b = *reinterpret_cast<const double2*>(PuI + (b2 ^ (8 * c + 2 * j)));
-            c2[c][2 * j] = b.x, c2[c][2 * j + 1] = b.y;
+            const double2 a = *reinterpret_cast<const double2*>(PuI + (bf ^ (8 * q + 2 * j)));
+            f[q][2 * j] = a.x, f[q][2 * j + 1] = a.y;
+            const double2 b = *reinterpret_cast<const double2*>(PuI + (bg ^ (8 * q + 2 * j)));
+            g[q][2 * j] = b.x, g[q][2 * j + 1] = b.y;
           }
-        h8p::up_fold([&](int c, int q) { return c1[c][q]; }, [&](int c, int q) { return c2[c][q]; }, xn, up);
+        double hf[4];
+        h8p::first_halves(f, xf, hf);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // hand-over second halves after the partner's first halves
+          double acc = __shfl_xor_sync(0xffffffffu, hf[q], 1);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc = acc + g[q][c] * xf[4 + c];
+          hs[q] = acc;
+        }
+        double xn[8];
+        get(vbuf, nf0, nf1, xn);
+        get(vbuf, nf2, nf3, xn + 4);
+        // up_r = sum_c U(r, c) x_{i+1}[c]: first halves from U(4h + q, c < 4), second from U(4(1-h) + q, 4 + c)
+        h8p::up_fold([&](int c, int q) { return h8p::sel(h, g[c][q], f[c][q]); },
+                     [&](int c, int q) { return h8p::sel(h, f[c][q], g[c][q]); }, xn, up);
       }
+      put(xbuf, ho0, ho1, hs);
+      __syncthreads();  // hand-overs published
       get(xbuf, my0, my1, low);
       finish(own, low, up, out);
     };
@@ -574,12 +609,12 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
 #endif
 }
 
-template <int MAXT, bool PREFETCH>
+template <int MAXT, bool PREFETCH, bool CW = false>
 __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8p(View v, const int* __restrict__ work,
                                                         const int* __restrict__ n_work, int* __restrict__ counter,
                                                         double* __restrict__ sol_all, double epsilon,
                                                         int max_iters_cfg) {
-  h8p_body<MAXT, PREFETCH>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
+  h8p_body<MAXT, PREFETCH, CW>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
 }
 
 }  // namespace docp_dev

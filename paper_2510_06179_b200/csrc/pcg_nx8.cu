@@ -12,6 +12,8 @@
 
 namespace docp_host {
 
+static bool force_variant(const char* name);
+
 template <bool PAR, bool RES>
 int launch_h8(docp_batch* b, const PcgPlan& pl, const int* list, const int* count, int n_hint, double* sol, double eps,
               int max_iters) {
@@ -122,8 +124,10 @@ static int launch_h8s(docp_batch* b, const int* list, const int* count, int n_hi
 template <bool PREFETCH>
 static int launch_h8p(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
                       int max_iters) {
-  auto kern = pcg_kernel_h8p<256, PREFETCH>;
-  const int threads = (2 * b->d.nb + 31) / 32 * 32;
+  // a spare eighth warp folds the block dots (T <= 111; DOCP_PCG_VARIANT=h8p_nocw: every warp does)
+  const bool cw = 2 * b->d.nb <= 32 * CW_WARP && !force_variant("h8p_nocw");
+  auto kern = cw ? pcg_kernel_h8p<256, PREFETCH, true> : pcg_kernel_h8p<256, PREFETCH, false>;
+  const int threads = cw ? 256 : (2 * b->d.nb + 31) / 32 * 32;
   if (threads > 256) return -1;
   const size_t smem = h8p_smem_doubles<PREFETCH>(b->d) * sizeof(double);
   int max_optin = 0;
