@@ -266,7 +266,7 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
 #ifdef DOCP_H8P_CLOCK
 /// A/B builds only: cycles of pcg_kernel_h8p's thread 0 per phase, summed over launches (then reset).
 extern "C" int docp_h8p_clock(unsigned long long* out) {
-  if (cudaMemcpyFromSymbol(out, docp_dev::g_h8p_clk, 12 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  if (cudaMemcpyFromSymbol(out, docp_dev::g_h8p_clk, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
   static const unsigned long long zero[16] = {0};
   return cudaMemcpyToSymbol(docp_dev::g_h8p_clk, zero, sizeof zero) != cudaSuccess;
 }
