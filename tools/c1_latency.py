@@ -41,6 +41,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=300)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--profile", action="store_true", help="per-kernel device times of one call (no-graph runs)")
     args = ap.parse_args()
     import paper_2510_06179_b200 as D
     import pyoracle as po
@@ -88,6 +89,13 @@ def main():
         gpu()
         out[f"gpu_{tag}_kernels_per_call"] = D.kernel_launches() - l0_
         out[f"gpu_{tag}_us"], out[f"gpu_{tag}_p90_us"] = median_us(gpu, args.reps)
+        if args.profile and not graphs:  # where one call's device time goes
+            b.profile_begin()
+            gpu()
+            p = b.profile_end()
+            out[f"gpu_{tag}_profile"] = {"kernels": {k: v for k, v in p["kernels"].items() if v["launches"]},
+                                          "pcg_iterations": p["pcg_iterations"], "pcg_solves": p["pcg_solves"],
+                                          "span_ms": p["span_ms"], "gap_ms": p["gap_ms"]}
     print(json.dumps(out))
     if args.json:
         with open(args.json, "w") as fh:
