@@ -970,11 +970,11 @@ int docp_il_epoch(docp_batch* b, const docp_sqp_config* cfg, const double* weigh
                                                                         b->counts + 4);
   } else {
     const int cols = 1 + learn_size;
-    const int ctas = (cols + kIlSumThreads - 1) / kIlSumThreads;
-    const int ncol = std::min(kIlSumThreads, cols);
-    // as few staging phases as 160 KB of shared memory allows
-    const int rows = std::max(1, std::min(b->B, (160 * 1024 / 8) / ncol - 1));
-    const size_t smem = static_cast<size_t>(rows | 1) * ncol * sizeof(double);
+    const int ctas = (cols + kIlSumCols - 1) / kIlSumCols;
+    const int ncol = std::min(kIlSumCols, cols);
+    // two staging buffers in 192 KB of shared memory
+    const int rows = std::max(1, std::min(b->B, (96 * 1024 / 8) / ncol - 1));
+    const size_t smem = 2 * static_cast<size_t>(rows | 1) * ncol * sizeof(double);
     CUDA_TRY(cudaFuncSetAttribute(il_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     il_sum_kernel<<<ctas, kIlSumThreads, smem, b->stream>>>(b->v, learn_start, learn_size, rows, loss_sum, grad_sum,
                                                             b->counts + 4);

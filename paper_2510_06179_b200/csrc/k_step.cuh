@@ -504,10 +504,12 @@ __global__ void __launch_bounds__(kIlLossThreads) il_loss_kernel(View v, const d
 
 /// Fixed-order (instance order) sums of the epoch (train.hpp:126-131). Column
 /// 0 is the loss, column 1 + i the i-th learnable gradient entry; CTA c owns
-/// columns [c * kIlSumThreads, ...). It stages `rows` instances of its columns
-/// in shared memory (coalesced, all loads in flight), then thread k folds its
-/// column in instance order.
+/// columns [c * kIlSumCols, ...). Lane k of warp 0 folds column k in instance
+/// order (one dependent chain per column, all columns side by side in one
+/// instruction stream) from a shared-memory phase of `rows` instances, while
+/// warps 1.. stage the next phase into the other buffer.
 constexpr int kIlSumThreads = 256;
+constexpr int kIlSumCols = 32;
 /// A demonstration whose solve or backward failed contributes nothing (its
 /// loss and gradient rows are stale); column 0's pass counts it into
 /// fails[0] and the smallest such index into fails[1] (docp_il_failures), so
@@ -524,28 +526,51 @@ __device__ __forceinline__ bool il_row_ok(const View& v, long p, int col, int* f
 __global__ void __launch_bounds__(kIlSumThreads) il_sum_kernel(View v, int learn_start, int learn_size, int rows,
                                                                double* __restrict__ loss_sum,
                                                                double* __restrict__ grad_sum, int* fails) {
-  extern __shared__ double stage_buf[];  // [ncol][ld]: column-major, odd leading dimension
-  const int c0 = blockIdx.x * kIlSumThreads;
-  const int ncol = min(kIlSumThreads, 1 + learn_size - c0);
-  const int ld = rows | 1;  // the folding threads walk their columns on distinct banks
-  const int k = threadIdx.x;
-  double acc = 0.0;
-  for (int p0 = 0; p0 < v.B; p0 += rows) {
+  extern __shared__ double stage_buf[];  // [2][ncol][ld]: column-major, odd leading dimension
+  const int c0 = blockIdx.x * kIlSumCols;
+  const int ncol = min(kIlSumCols, 1 + learn_size - c0);
+  const int ld = rows | 1;  // the folding lanes walk their columns on distinct banks
+  const int tid = threadIdx.x, k = tid;
+  const int nth = v.d.nth;
+  // rows [p0, p0 + n) of every column into buffer `which` (warps 1..)
+  auto stage = [&](int p0, double* buf) {
     const int n = min(rows, v.B - p0);
-    __syncthreads();
-    for (int g = threadIdx.x; g < n * ncol; g += blockDim.x) {
-      const int j = g / ncol, c = g - j * ncol;
+    for (int j = tid - 32; j < n; j += kIlSumThreads - 32) {
       const long p = p0 + j;
-      stage_buf[c * ld + j] = !il_row_ok(v, p, c0 + c, fails) ? 0.0
-                              : c0 + c == 0                 ? v.loss[p]
-                                                            : v.grad[p * v.d.nth + learn_start + c0 + c - 1];
+      const bool ok = il_row_ok(v, p, c0, fails);
+      const double* gp = v.grad + p * nth + learn_start - 1;
+#pragma unroll 4
+      for (int c = 0; c < ncol; ++c)
+        buf[c * ld + j] = !ok ? 0.0 : c0 + c == 0 ? v.loss[p] : gp[c0 + c];
+    }
+  };
+  double acc = 0.0;
+  if (tid >= 32) stage(0, stage_buf);
+  __syncthreads();
+  for (int p0 = 0, ph = 0; p0 < v.B; p0 += rows, ph ^= 1) {
+    if (tid >= 32) {
+      if (p0 + rows < v.B) stage(p0 + rows, stage_buf + (ph ^ 1) * ncol * ld);
+    } else if (k < ncol) {
+      // instance order (train.hpp:126-131); blocks of 16 loaded one block ahead
+      const double* col = stage_buf + ph * ncol * ld + k * ld;
+      const int n = min(rows, v.B - p0), n16 = n & ~15;
+      double A[16], Bv[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) A[t] = t < n16 ? col[t] : 0.0;
+      for (int j = 0; j < n16; j += 32) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) Bv[t] = j + 16 + t < n16 ? col[j + 16 + t] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) acc = acc + A[t];
+        if (j + 16 >= n16) break;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) A[t] = j + 32 + t < n16 ? col[j + 32 + t] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) acc = acc + Bv[t];
+      }
+      for (int j = n16; j < n; ++j) acc = acc + col[j];
     }
     __syncthreads();
-    if (k < ncol) {
-      const double* col = stage_buf + k * ld;
-#pragma unroll 8
-      for (int j = 0; j < n; ++j) acc = acc + col[j];  // instance order (train.hpp:126-131)
-    }
   }
   if (k < ncol) {
     if (c0 + k == 0) *loss_sum = acc;
