@@ -1103,8 +1103,9 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   char fast[128];
   const int s8 = d.nx == 8 ? h8s_variant_for(d, dev) : 0;
   if (h4f_fits(d, dev)) snprintf(fast, sizeof fast, "pcg_kernel_h4f(resident)");
-  else if (s8 >= 2) snprintf(fast, sizeof fast, "pcg_kernel_h8s<%d,no-prefetch>(resident); uploaded systems %s",
-                             s8 == 2 ? 256 : 384, cl == 2 ? "pcg_kernel_h8f(cluster2)" : "pcg_kernel_h8f");
+  else if (s8 >= 2) snprintf(fast, sizeof fast, "pcg_kernel_h8s<%d,no-prefetch%s>(resident); uploaded systems %s",
+                             s8 == 2 ? 256 : 384, s8 == 4 ? ",-S in smem" : "",
+                             cl == 2 ? "pcg_kernel_h8f(cluster2)" : "pcg_kernel_h8f");
   else if (cl == 1) snprintf(fast, sizeof fast, "%s(resident)",
                            d.nx == 8 ? "pcg_kernel_h8s; uploaded systems pcg_kernel_h8r" : fk);
   else if (cl > 1) snprintf(fast, sizeof fast, "%s(cluster%d,resident)", fk, cl);

@@ -83,10 +83,10 @@ __device__ __forceinline__ void sym_times(const Sym& m, const double* xf, const 
 /// Dynamic shared memory of pcg_kernel_h8s (doubles). PREFETCH: Phi^-1 of the
 /// current problem plus a staging area for the next problem's -S; otherwise
 /// one record-sized region that takes -S, then Phi^-1, of the current problem.
-template <int MAXT, bool PREFETCH>
+template <int MAXT, bool PREFETCH, bool SD_SMEM = false>
 __host__ __device__ inline long h8s_smem_doubles(const Dims& d) {
   constexpr int NWS = MAXT <= 256 ? 8 : 16;
-  return (PREFETCH ? 4L : 2L) * d.nb * 64 + 2L * (d.nb + 2) * 8 + 3 * NWS;
+  return (PREFETCH ? 4L : SD_SMEM ? 3L : 2L) * d.nb * 64 + 2L * (d.nb + 2) * 8 + 3 * NWS;
 }
 
 /// MAXT = 256: 255 registers per thread; with PREFETCH = false (T <= 127) the
@@ -109,7 +109,11 @@ __device__ unsigned long long g_h8s_clk[16];
 /// iteration (rows 4h..4h+3, as U_i) instead of being held in registers:
 /// 36 registers fewer, for the wide form whose 9-12 warps cap every thread
 /// at 168 registers (an SMSP then holds three warps).
-template <int MAXT, bool PREFETCH, bool PD_SMEM = false>
+/// SD_SMEM (with PD_SMEM, no prefetch): the -S diagonal blocks stay in a
+/// third shared-memory region as well, so only L_i's rows stay in registers:
+/// the > 8-warp forms (168 registers per thread) then run without spilling
+/// where three regions fit (T <= 134).
+template <int MAXT, bool PREFETCH, bool PD_SMEM = false, bool SD_SMEM = false>
 __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, const int* __restrict__ n_work,
                                          int* __restrict__ counter, double* __restrict__ sol_all, double epsilon,
                                          int max_iters_cfg) {
@@ -132,13 +136,16 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
 #endif
 
   constexpr int NWS = MAXT <= 256 ? 8 : 16;  // warp slots per dot
+  static_assert(!SD_SMEM || (PD_SMEM && !PREFETCH), "SD_SMEM is a no-prefetch, PD_SMEM form");
   double* sPd = sm_pcg;            // [R] Phi^-1 diagonal blocks (current problem)
   double* sPu = sPd + R * 64;      // [R] Phi^-1 super blocks
+  double* sSr = sPu + R * 64;      // SD_SMEM: [R] -S diagonal blocks, resident
   // -S diagonal / sub blocks: the next problem's (staging) or, without the
-  // prefetch, the current problem's in the same region as Phi^-1
-  double* sNd = PREFETCH ? sPu + R * 64 : sPd;
-  double* sNs = sNd + R * 64;
-  double* vbuf = sPu + (PREFETCH ? 3 : 1) * R * 64;  // [R + 2] x_i halves (slot = row + 1)
+  // prefetch, the current problem's in the same region as Phi^-1 (SD_SMEM:
+  // the diagonal ones straight into their resident region)
+  double* sNd = PREFETCH ? sPu + R * 64 : SD_SMEM ? sSr : sPd;
+  double* sNs = SD_SMEM ? sPd : sNd + R * 64;
+  double* vbuf = sPu + (PREFETCH ? 3 : SD_SMEM ? 2 : 1) * R * 64;  // [R + 2] x_i halves (slot = row + 1)
   double* xbuf = vbuf + (R + 2) * 8;
   double* red = xbuf + (R + 2) * 8;  // [3][NWS] dot partials
 
@@ -322,7 +329,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       }
     }
     mbar_wait(&s_bar[0], phase);
-    h8s::load_sym(NdI, ib, h, sd);
+    if constexpr (!SD_SMEM) h8s::load_sym(NdI, ib, h, sd);
     h8f::load_rows(NsI, bs, so);
     __syncthreads();  // staging area consumed; s_next / s_pidx read; Phi^-1 reads of the previous problem done
     phase ^= 1;
@@ -356,7 +363,13 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       gather(xr, xf);
       put(vbuf, my0, my1, xr);
       H8S_CLK(12);
-      h8s::sym_times(sd, xf, xr, h, own);
+      if constexpr (SD_SMEM) {
+        double2 dd[8][2];
+        h8f::load_rows(NdI, bs, dd);
+        rows_times(dd, xf, own);
+      } else {
+        h8s::sym_times(sd, xf, xr, h, own);
+      }
       H8S_CLK(13);
       rows_times(so, xf, hand);  // L_i x_i
       put(xbuf, pv0, pv1, hand);  // slot i (see pp0 above)
@@ -509,6 +522,13 @@ __global__ void __maxnreg__(168)
     pcg_kernel_h8s_wide(View v, const int* __restrict__ work, const int* __restrict__ n_work,
                         int* __restrict__ counter, double* __restrict__ sol_all, double epsilon, int max_iters_cfg) {
   h8s_body<384, false, true>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
+}
+
+/// The same with -S_ii in shared memory too (T <= 134): no spills at 168.
+__global__ void __maxnreg__(168)
+    pcg_kernel_h8s_wide_sd(View v, const int* __restrict__ work, const int* __restrict__ n_work,
+                           int* __restrict__ counter, double* __restrict__ sol_all, double epsilon, int max_iters_cfg) {
+  h8s_body<384, false, true, true>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
 }
 
 }  // namespace docp_dev

@@ -96,13 +96,13 @@ static int launch_h8r(docp_batch* b, const int* list, const int* count, int n_hi
 /// FAST, one CTA per problem, device-assembled (symmetric) diagonal blocks:
 /// pcg_kernel_h8s (both diagonal blocks in registers). Returns -1 (nothing
 /// launched) when the variant does not fit this shape.
-template <int MAXT, bool PREFETCH>
+template <int MAXT, bool PREFETCH, bool SD = false>
 static int launch_h8s(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
                       int max_iters) {
-  auto kern = MAXT == 384 ? pcg_kernel_h8s_wide : pcg_kernel_h8s<MAXT, PREFETCH>;
+  auto kern = MAXT == 384 ? (SD ? pcg_kernel_h8s_wide_sd : pcg_kernel_h8s_wide) : pcg_kernel_h8s<MAXT, PREFETCH>;
   const int threads = (2 * b->d.nb + 31) / 32 * 32;
   if (threads > MAXT) return -1;
-  const size_t smem = h8s_smem_doubles<MAXT, PREFETCH>(b->d) * sizeof(double);
+  const size_t smem = h8s_smem_doubles<MAXT, PREFETCH, SD>(b->d) * sizeof(double);
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device);
   if (smem + 256 > static_cast<size_t>(max_optin)) return -1;
@@ -188,6 +188,9 @@ int h8s_variant_for(const Dims& d, int device) {
   const int threads = (2 * d.nb + 31) / 32 * 32;
   if (threads <= 256 && h8s_smem_doubles<256, true>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 1;
   if (threads <= 256 && h8s_smem_doubles<256, false>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 2;
+  if (threads <= 384 && h8s_smem_doubles<384, false, true>(d) * 8 + 256 <= static_cast<long>(max_optin) &&
+      !std::getenv("DOCP_H8S_NO_SD"))
+    return 4;
   if (threads <= 384 && h8s_smem_doubles<384, false>(d) * 8 + 256 <= static_cast<long>(max_optin)) return 3;
   return 0;
 }
@@ -237,6 +240,7 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
       case 1: rc = launch_h8s<256, true>(b, list, count, n_hint, sol, eps, max_iters); break;
       case 2: rc = launch_h8s<256, false>(b, list, count, n_hint, sol, eps, max_iters); break;
       case 3: rc = launch_h8s<384, false>(b, list, count, n_hint, sol, eps, max_iters); break;
+      case 4: rc = launch_h8s<384, false, true>(b, list, count, n_hint, sol, eps, max_iters); break;
       default: break;
     }
     if (rc != -1) return rc;

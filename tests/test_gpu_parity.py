@@ -665,7 +665,7 @@ def test_pcg_breakdown_all_kernels(D, nx, nu, T):
 
 
 @pytest.mark.parametrize("nx,nu,T", [(8, 4, 1), (8, 4, 2), (8, 4, 30), (8, 4, 100), (8, 4, 113), (8, 4, 120),
-                                     (8, 4, 127), (8, 4, 128), (8, 4, 143), (8, 4, 160),
+                                     (8, 4, 127), (8, 4, 128), (8, 4, 134), (8, 4, 135), (8, 4, 143), (8, 4, 160),
                                      (8, 4, 191)])
 def test_fast_nx8_kernels_agree(D, nx, nu, T, monkeypatch):
     """The n_x = 8 single-CTA FAST kernels: pcg_kernel_h8r (-S in registers)
