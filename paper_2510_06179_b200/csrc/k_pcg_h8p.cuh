@@ -163,9 +163,13 @@ __device__ __forceinline__ void up_fold(C1 c1, C2 c2, const double* xn, double* 
 /// Dynamic shared memory of pcg_kernel_h8p (doubles): as h8s, plus the block
 /// dots (nb, even) and nothing else; the rare eta < 0 path folds the norms
 /// in the vector buffers.
+/// Block-dot slots: nb rounded up to 16, plus two blocks of 16, all past nb
+/// zero (the fold warp reads whole 16-blocks one block ahead, unguarded).
+__host__ __device__ inline long h8p_seg_doubles(int nb) { return ((nb + 15) & ~15) + 32; }
+
 template <bool PREFETCH>
 __host__ __device__ inline long h8p_smem_doubles(const Dims& d) {
-  return (PREFETCH ? 4L : 2L) * d.nb * 64 + 2L * (d.nb + 2) * 8 + ((d.nb + 1) & ~1);
+  return (PREFETCH ? 4L : 2L) * d.nb * 64 + 2L * (d.nb + 2) * 8 + h8p_seg_doubles(d.nb);
 }
 
 #ifdef DOCP_H8P_CLOCK
@@ -213,7 +217,7 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
   double* sNs = sNd + R * 64;
   double* vbuf = sPu + (PREFETCH ? 3 : 1) * R * 64;  // [R + 2] x_i (slot = row + 1)
   double* xbuf = vbuf + (R + 2) * 8;                 // [R + 2] hand-overs
-  double* seg = xbuf + (R + 2) * 8;                  // [nb] block dots
+  double* seg = xbuf + (R + 2) * 8;                  // [h8p_seg_doubles] block dots, zero past nb
 
   const int ib = act ? il : nb - 1;
   const int io = has_next ? il : 0;
@@ -247,6 +251,7 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
     if (bo) tma_bulk_g2s(sNs, rec + d.s_sub, bo, &s_bar[0]);
   };
 
+  for (int k = nb + tid; k < h8p_seg_doubles(nb); k += blockDim.x) seg[k] = 0.0;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -311,25 +316,27 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
 #ifdef DOCP_H8P_CLOCK
           const long long tc0 = clock64();
 #endif
-          // front-padded with +0.0 to a multiple of 16 (exact: the fold
-          // starts from 0.0 anyway, and 0.0 + 0.0 = +0.0), so the adds run
-          // without per-element predicates (a predicated add puts a select
-          // into the dependent chain: 13 instead of 8 cycles per element)
-          const int pad = (16 - (nb & 15)) & 15, total = nb + pad;
-          auto ld = [&](int k) { return k >= pad && k < total ? seg[k - pad] : 0.0; };
-          double A[16], Bv[16], acc = 0.0;
+          // whole blocks of 16, zero-padded at the end in shared memory
+          // (exact: a fold seeded with +0.0 is never -0.0, so acc + 0.0 =
+          // acc), two LDS.128 per four entries, one block loaded ahead: no
+          // predicate, select or branch inside a block of the dependent
+          // chain (a per-group exit test costs more than the padding adds)
+          const double2* sg = reinterpret_cast<const double2*>(seg);
+          const int nblk = (nb + 15) >> 4;
+          double2 A[8], Bv[8];
+          double acc = 0.0;
 #pragma unroll
-          for (int t = 0; t < 16; ++t) A[t] = ld(t);
-          for (int k = 0; k < total; k += 32) {
+          for (int t = 0; t < 8; ++t) A[t] = sg[t];
+          for (int k = 0; k < nblk; k += 2) {
 #pragma unroll
-            for (int t = 0; t < 16; ++t) Bv[t] = ld(k + 16 + t);
+            for (int t = 0; t < 8; ++t) Bv[t] = sg[8 * (k + 1) + t];
 #pragma unroll
-            for (int t = 0; t < 16; ++t) acc = acc + A[t];
-            if (k + 16 >= total) break;
+            for (int t = 0; t < 8; ++t) acc = (acc + A[t].x) + A[t].y;
+            if (k + 1 >= nblk) break;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) A[t] = ld(k + 32 + t);
+            for (int t = 0; t < 8; ++t) A[t] = sg[8 * (k + 2) + t];
 #pragma unroll
-            for (int t = 0; t < 16; ++t) acc = acc + Bv[t];
+            for (int t = 0; t < 8; ++t) acc = (acc + Bv[t].x) + Bv[t].y;
           }
           s_dot = acc;
 #ifdef DOCP_H8P_CLOCK
