@@ -195,7 +195,7 @@ int h8s_variant_for(const Dims& d, int device) {
   return 0;
 }
 
-/// Smallest cluster (1, 2, 4, 8) whose per-CTA share of the blocks fits in
+/// Smallest cluster (1 .. 8) whose per-CTA share of the blocks fits in
 /// shared memory with at most 128 block rows per CTA; 0 if none.
 int h8f_cluster_for(const Dims& d, int device) {
   if (d.nx != 8) return 0;
@@ -203,7 +203,7 @@ int h8f_cluster_for(const Dims& d, int device) {
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   int min_cl = 1;  // DOCP_H8F_CLUSTER=c: A/B override, smallest cluster size tried
   if (const char* e = std::getenv("DOCP_H8F_CLUSTER")) min_cl = std::atoi(e);
-  for (int cl : {1, 2, 4, 8}) {
+  for (int cl : {1, 2, 3, 4, 5, 6, 7, 8}) {
     if (cl > 1 && (cl - 1) * h8f_rows(d, cl) >= d.nb) break;  // every CTA must own a row
     if (cl < min_cl) continue;
     if (h8f_rows(d, cl) <= 128 && h8f_smem_doubles(d, cl, false) * 8 + 64 <= static_cast<long>(max_optin)) return cl;
@@ -251,7 +251,11 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
         if (force_variant("h8f")) return launch_h8f_cl<1>(b, list, count, n_hint, sol, eps, max_iters);
         return launch_h8r(b, list, count, n_hint, sol, eps, max_iters);
       case 2: return launch_h8f_cl<2>(b, list, count, n_hint, sol, eps, max_iters);
+      case 3: return launch_h8f_cl<3>(b, list, count, n_hint, sol, eps, max_iters);
       case 4: return launch_h8f_cl<4>(b, list, count, n_hint, sol, eps, max_iters);
+      case 5: return launch_h8f_cl<5>(b, list, count, n_hint, sol, eps, max_iters);
+      case 6: return launch_h8f_cl<6>(b, list, count, n_hint, sol, eps, max_iters);
+      case 7: return launch_h8f_cl<7>(b, list, count, n_hint, sol, eps, max_iters);
       case 8: return launch_h8f_cl<8>(b, list, count, n_hint, sol, eps, max_iters);
       default: break;
     }

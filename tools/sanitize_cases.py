@@ -23,7 +23,9 @@ CASES = {
     "h8r": (8, 4, 30, 3, {"DOCP_PCG_VARIANT": "h8r"}, ("fast",)),
     "h8f_cl1": (8, 4, 30, 3, {"DOCP_PCG_VARIANT": "h8f"}, ("fast",)),
     "h8f_cl2": (8, 4, 60, 2, {"DOCP_PCG_VARIANT": "h8f", "DOCP_H8F_CLUSTER": "2"}, ("fast",)),
+    "h8f_cl3": (8, 4, 60, 2, {"DOCP_PCG_VARIANT": "h8f", "DOCP_H8F_CLUSTER": "3"}, ("fast",)),
     "h8f_cl4": (8, 4, 60, 2, {"DOCP_PCG_VARIANT": "h8f", "DOCP_H8F_CLUSTER": "4"}, ("fast",)),
+    "h8f_cl6": (8, 4, 60, 2, {"DOCP_PCG_VARIANT": "h8f", "DOCP_H8F_CLUSTER": "6"}, ("fast",)),
     "h8f_cl4_nodbuf": (8, 4, 400, 1, {}, ("fast",)),  # R = 101: the barrier form (no second buffer pair)
     "h8_fast": (8, 4, 30, 3, {"DOCP_PCG_VARIANT": "h8"}, ("fast",)),
     "h8p": (8, 4, 30, 3, {}, ("parity",)),
