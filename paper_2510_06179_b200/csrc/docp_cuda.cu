@@ -1123,3 +1123,12 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
 }
 
 }  // extern "C"
+
+#ifdef DOCP_K1_CLOCK
+/// A/B builds only: cycles of assemble_kernel_t's thread 0 per phase, summed over launches (then reset).
+extern "C" int docp_k1_clock(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, docp_dev::g_k1_clk, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  static const unsigned long long zero[16] = {0};
+  return cudaMemcpyToSymbol(docp_dev::g_k1_clk, zero, sizeof zero) != cudaSuccess;
+}
+#endif

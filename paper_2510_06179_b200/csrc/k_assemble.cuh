@@ -20,6 +20,19 @@
 namespace docp_dev {
 
 constexpr int kAsmThreads = 256;
+
+#ifdef DOCP_K1_CLOCK
+// phase timing of thread 0 in assemble_kernel_t (A/B builds only: nvcc -DDOCP_K1_CLOCK)
+__device__ unsigned long long g_k1_clk[16];
+#define K1_CLK(k)                         \
+  if (threadIdx.x == 0) {                 \
+    const long long t_ = clock64();       \
+    k1clk[k] += t_ - k1last;              \
+    k1last = t_;                          \
+  }
+#else
+#define K1_CLK(k)
+#endif
 constexpr int kAsmWarps = kAsmThreads / kWarp;
 
 // ranks that order errors exactly as the reference raises them
@@ -594,13 +607,18 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
   };
 
   const bool stage_in = d.nz + d.nth <= NG * Lay::GBUF;
+#ifdef DOCP_K1_CLOCK
+  long long k1clk[16] = {0}, k1last = clock64();
+#endif
   for (int w = blockIdx.x; w < *n_work; w += gridDim.x) {
     const int p = work[w];
+    K1_CLK(11);
     // z / theta staged in the group buffers (free until phase B) when they fit
     if (!phase_linearize<NX, NU, DR>(v, p, eps_pd, do_schur, sh, stage_in ? sm_asm : nullptr)) {
       __syncthreads();
       continue;
     }
+    K1_CLK(0);
     const double* lq = v.lq + static_cast<long>(p) * d.nb * NX;
     const double* lr = v.lr + static_cast<long>(p) * T * NU;
     const double* qdp = v.qd + static_cast<long>(p) * d.nb * NX;
@@ -641,6 +659,7 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
 #pragma unroll
         for (int k = l; k < NX * NU; k += NX) sB[ix(k % NX, k / NX)] = Bt[k];
         __syncwarp(gmask);
+        K1_CLK(1);
         // M1(k, l) = (A(l,k)/lq_k)/lq_k ; M2(k, l) = (B(l,k)/lr_k)/lr_k
         double c3;
         if constexpr (FAST) {  // lane k scales column k of A (of B) by 1/q_k (1/r_k)
@@ -662,6 +681,7 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
             dq = (1.0 / lqt[l]) / lqt[l];
           }
           __syncwarp(gmask);
+          K1_CLK(2);
           // column l of chi = A M1 + B M2 + A+ Q+^-1 A+'  and of phi_t = A Q_t^-1
 #pragma unroll
           for (int i = 0; i < NX; ++i) {
@@ -681,6 +701,7 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
             sC[ix(i, l)] = (a + b) + (i == l ? c3 : 0.0);
           }
           __syncwarp(gmask);  // B_t / M2 are dead: sO takes their place
+          K1_CLK(3);
 #pragma unroll
           for (int i = 0; i < NX; ++i) stage(t, i, l, sA[ix(i, l)] * dq);
           flush(Ss, t);
@@ -692,6 +713,7 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
             sM1[ix(i, l)] = 0.0;  // becomes L
           }
           flush(Sd, t + 1);
+          K1_CLK(4);
           // Cholesky of chi_t (eigen_lite LLT): lane l computes row l
           double* sL = sM1;
           bool failed = false;
@@ -722,6 +744,7 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
             }
             __syncwarp(gmask);
           }
+          K1_CLK(5);
           if (failed) {
             if (l == 0) atomicMin(&sh.rank_chi, t);
             __syncwarp(gmask);
@@ -739,7 +762,17 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
 #pragma unroll
                 for (int j = 1; j < i; ++j) s = FAST ? fma(sL[ix(i, j)], x[j], s) : s + sL[ix(i, j)] * x[j];
               }
-              x[i] = FAST ? ((i == l ? 1.0 : 0.0) - s) * sL[ix(i, i)] : ((i == l ? 1.0 : 0.0) - s) / sL[ix(i, i)];
+              if constexpr (FAST) {
+                x[i] = ((i == l ? 1.0 : 0.0) - s) * sL[ix(i, i)];
+              } else {
+                // a zero numerator (rows above the unit entry of column l)
+                // is its own quotient: L(i, i) = sqrt(pivot) > 0, so 0 / L is
+                // the same signed zero; skipping the division keeps those
+                // lanes off its slow path (taken for zero numerators)
+                const double num = (i == l ? 1.0 : 0.0) - s;
+                x[i] = num;
+                if (num != 0.0) x[i] = num / sL[ix(i, i)];
+              }
             }
 #pragma unroll
             for (int i = NX - 1; i >= 0; --i) {
@@ -749,13 +782,20 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
 #pragma unroll
                 for (int j = i + 2; j < NX; ++j) s = FAST ? fma(sL[ix(j, i)], x[j], s) : s + sL[ix(j, i)] * x[j];
               }
-              x[i] = FAST ? (x[i] - s) * sL[ix(i, i)] : (x[i] - s) / sL[ix(i, i)];
+              if constexpr (FAST) {
+                x[i] = (x[i] - s) * sL[ix(i, i)];
+              } else {
+                const double num = x[i] - s;  // zero numerators as above
+                x[i] = num;
+                if (num != 0.0) x[i] = num / sL[ix(i, i)];
+              }
             }
             __syncwarp(gmask);  // everyone is done reading chi (sC) before it becomes X
 #pragma unroll
             for (int i = 0; i < NX; ++i) sX[ix(i, l)] = x[i];
           }
           __syncwarp(gmask);
+          K1_CLK(6);
 #pragma unroll
           for (int i = 0; i < NX; ++i) {
             const double pv = 0.5 * (sX[ix(i, l)] + sX[ix(l, i)]);
@@ -765,9 +805,11 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
           flush(Pd, t + 1);
 #pragma unroll
           for (int i = 0; i < NX; ++i) sM1[ix(i, l)] = sA[ix(i, l)] * dq;  // sub_t (= the Ss_t block); L is dead
+          K1_CLK(7);
         }  // chi_t factorised
       }  // stage exists
       __syncthreads();
+      K1_CLK(8);
 
       // ---------------- phase C: stair off-diagonal (-D_t phi_t') D_{t+1} (schur.hpp:169-179)
       if (ok) {
@@ -805,13 +847,19 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
           for (int i = 0; i < NX; ++i) carry[((t0 / NG) & 1) * Lay::P2 + ix(i, l)] = sD[ix(i, l)];
         }
       }
+      K1_CLK(9);
       __syncthreads();
+      K1_CLK(10);
     }
     if (sh.rank_chi != kNoError) {
       if (tid == 0) set_status(v.status + p, DOCP_NUMERICAL, DOCP_AT_CHOL_CHI, sh.rank_chi);
     }
     __syncthreads();  // sh is re-initialised by the next problem
   }
+#ifdef DOCP_K1_CLOCK
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 12; ++k) atomicAdd(&g_k1_clk[k], static_cast<unsigned long long>(k1clk[k]));
+#endif
 }
 
 /// Solve Q_t x = b for the diagonal Cholesky factor l: (b / l) / l.
