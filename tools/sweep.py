@@ -34,6 +34,7 @@ from paper_2510_06179_b200 import _lib as L  # noqa: E402
 
 POOL = 65536
 CONVEX = False
+MODE = "fast"
 
 
 def hbm_peak():
@@ -67,7 +68,7 @@ def run(T, B, reps, pool_cache, chunk=65536):
     th_dev = torch.tensor(th, device="cuda")
     g = torch.tensor(np.random.default_rng(0).standard_normal((C, nz)) * 1e-2, device="cuda")
     b.upload(L.F_LOSS_GRAD_Z, g)
-    cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode="fast"))
+    cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(epsilon=1e-12, mode=MODE))
     zeros_z = torch.zeros((C, nz), dtype=torch.float64, device="cuda")
     zeros_l = torch.zeros((C, nl), dtype=torch.float64, device="cuda")
 
@@ -111,9 +112,10 @@ def main():
     ap.add_argument("--nu", type=int, default=4)
     ap.add_argument("--nx", type=int, default=8)
     ap.add_argument("--convex", action="store_true", help="random_convex_instance draws (domain-randomised weights)")
+    ap.add_argument("--mode", default="fast", choices=["fast", "parity", "fp32"], help="PCG arithmetic")
     a = ap.parse_args()
-    global NU, NX, CONVEX
-    NU, NX, CONVEX = a.nu, a.nx, a.convex
+    global NU, NX, CONVEX, MODE
+    NU, NX, CONVEX, MODE = a.nu, a.nx, a.convex, a.mode
     rows = []
     cache = {}
     for T in [int(x) for x in a.T.split(",")]:
@@ -124,7 +126,7 @@ def main():
             torch.cuda.empty_cache()
     if a.md:
         with open(a.md, "w") as fh:
-            fh.write("# Sweep — solve + gradient on one B200 (FAST, cold caches, median of %d)\n\n" % a.reps)
+            fh.write("# Sweep — solve + gradient on one B200 (%s, cold caches, median of %d)\n\n" % (MODE.upper(), a.reps))
             fh.write(f"Workload: `{'random_convex_instance' if CONVEX else 'random_linear_instance'}({NX}, {NU}, T)` "
                      "draws, `sqp_solve` (5 SQP iterations max, "
                      "eps 1e-12) + `backward_vjp` per problem. PCG GB/s = algorithmic bytes "
@@ -132,7 +134,8 @@ def main():
             fh.write("| T | B | problems/s | ms/step | PCG it/solve | PCG share | PCG GB/s | x HBM | PCG kernel |\n")
             fh.write("|---|---|---|---|---|---|---|---|---|\n")
             for r in rows:
-                kern = r["pcg_kernel"].split("fast=")[1].split(" ")[0]
+                kern = (r["pcg_kernel"].split("parity=")[1].split(";")[0].split(" fast=")[0] if MODE == "parity"
+                        else r["pcg_kernel"].split("fast=")[1].split(" ")[0])
                 fh.write(f"| {r['T']} | {r['B']} | {r['problems_per_s']:,.0f} | {r['ms_per_step']:.2f} | "
                          f"{r['pcg_iters_per_solve']:.1f} | {r['pcg_share']:.2f} | {r['pcg_algorithmic_GBps']:,.0f} | "
                          f"{r['pcg_frac_hbm']:.2f} | {kern} |\n")
