@@ -291,9 +291,35 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
       out[q] = acc;
     }
   };
+  // The block dots in index order from 0.0 (pcg.hpp:37-44), by one lane:
+  // whole blocks of 16, zero-padded at the end in shared memory (exact: a
+  // fold seeded with +0.0 is never -0.0, so acc + 0.0 = acc), two LDS.128 per
+  // four entries, one block loaded ahead: no predicate, select or branch
+  // inside a block of the dependent chain (a per-group exit test costs more
+  // than the padding adds)
+  auto fold_seg = [&]() -> double {
+    const double2* sg = reinterpret_cast<const double2*>(seg);
+    const int nblk = (nb + 15) >> 4;
+    double2 A[8], Bv[8];
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) A[t] = sg[t];
+    for (int k = 0; k < nblk; k += 2) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) Bv[t] = sg[8 * (k + 1) + t];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc = (acc + A[t].x) + A[t].y;
+      if (k + 1 >= nblk) break;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) A[t] = sg[8 * (k + 2) + t];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc = (acc + Bv[t].x) + Bv[t].y;
+    }
+    return acc;
+  };
   // block_dot (pcg.hpp:37-44): the 8-term fold of block i is cut after its
-  // 4th term (thread 0 -> thread 1); the block dots are then summed in index
-  // order, 0.0 first, by lane 0 of every warp (no second barrier).
+  // 4th term (thread 0 -> thread 1); the block dots are then folded by the
+  // spare warp's lane 0 (CW) or by lane 0 of every warp (no second barrier)
   auto dot = [&](const double* a, const double* b) -> double {
     double s = a[0] * b[0];
     s = s + a[1] * b[1];
@@ -316,28 +342,7 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
 #ifdef DOCP_H8P_CLOCK
           const long long tc0 = clock64();
 #endif
-          // whole blocks of 16, zero-padded at the end in shared memory
-          // (exact: a fold seeded with +0.0 is never -0.0, so acc + 0.0 =
-          // acc), two LDS.128 per four entries, one block loaded ahead: no
-          // predicate, select or branch inside a block of the dependent
-          // chain (a per-group exit test costs more than the padding adds)
-          const double2* sg = reinterpret_cast<const double2*>(seg);
-          const int nblk = (nb + 15) >> 4;
-          double2 A[8], Bv[8];
-          double acc = 0.0;
-#pragma unroll
-          for (int t = 0; t < 8; ++t) A[t] = sg[t];
-          for (int k = 0; k < nblk; k += 2) {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) Bv[t] = sg[8 * (k + 1) + t];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) acc = (acc + A[t].x) + A[t].y;
-            if (k + 1 >= nblk) break;
-#pragma unroll
-            for (int t = 0; t < 8; ++t) A[t] = sg[8 * (k + 2) + t];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) acc = (acc + Bv[t].x) + Bv[t].y;
-          }
+          const double acc = fold_seg();
           s_dot = acc;
 #ifdef DOCP_H8P_CLOCK
           atomicAdd(&g_h8p_clk[12], static_cast<unsigned long long>(clock64() - tc0));
@@ -352,26 +357,7 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
     }
     double acc = 0.0;
     if (lane == 0) {
-      // software-pipelined: the next 8 block dots are loaded while the current
-      // 8 are added, so the chain runs at the DADD latency (8 cycles)
-      const double2* sg = reinterpret_cast<const double2*>(seg);
-      const int n8 = nb >> 3;
-      double2 c0, c1, c2, c3;
-      if (n8 > 0) c0 = sg[0], c1 = sg[1], c2 = sg[2], c3 = sg[3];
-      for (int k = 0; k < n8; ++k) {
-        const int nx8 = k + 1 < n8 ? 4 * (k + 1) : 4 * k;
-        const double2 d0 = sg[nx8], d1 = sg[nx8 + 1], d2 = sg[nx8 + 2], d3 = sg[nx8 + 3];
-        acc = acc + c0.x;
-        acc = acc + c0.y;
-        acc = acc + c1.x;
-        acc = acc + c1.y;
-        acc = acc + c2.x;
-        acc = acc + c2.y;
-        acc = acc + c3.x;
-        acc = acc + c3.y;
-        c0 = d0, c1 = d1, c2 = d2, c3 = d3;
-      }
-      for (int k = 8 * n8; k < nb; ++k) acc = acc + seg[k];
+      acc = fold_seg();
     }
     const double tot = __shfl_sync(0xffffffffu, acc, 0);
     H8P_CLK(8);
