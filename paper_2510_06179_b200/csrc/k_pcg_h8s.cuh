@@ -129,7 +129,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   const bool act = i < nb;
   const bool has_next = act && i + 1 < nb;
   const bool has_prev = i > 0;
-  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   const int nwk = *n_work;
 #ifdef DOCP_H8S_CLOCK
   long long clk[16] = {0}, t_last = clock64();
