@@ -143,6 +143,8 @@ int h16f_cluster_for(const docp_dev::Dims& d, int device);
 int h8f_cluster_for(const docp_dev::Dims& d, int device);
 /// pcg_kernel_h8s variant for a device-assembled system (0: none; 1: T <= 113; 2: T <= 127; 3: T <= 191).
 int h8s_variant_for(const docp_dev::Dims& d, int device);
+int h8s_cluster_for(const docp_dev::Dims& d, int device);
+bool h8s_cluster_preferred(const docp_dev::Dims& d, int device);
 /// pcg_kernel_h8p (PARITY) variant for a device-assembled system (0: none; 1: prefetching; 2: no prefetch).
 int h8p_variant_for(const docp_dev::Dims& d, int device);
 DOCP_PCG_LAUNCHER(launch_pcg_nx8);

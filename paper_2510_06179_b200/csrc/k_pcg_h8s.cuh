@@ -83,10 +83,11 @@ __device__ __forceinline__ void sym_times(const Sym& m, const double* xf, const 
 /// Dynamic shared memory of pcg_kernel_h8s (doubles). PREFETCH: Phi^-1 of the
 /// current problem plus a staging area for the next problem's -S; otherwise
 /// one record-sized region that takes -S, then Phi^-1, of the current problem.
-template <int MAXT, bool PREFETCH, bool SD_SMEM = false>
+template <int MAXT, bool PREFETCH, bool SD_SMEM = false, int CL = 1>
 __host__ __device__ inline long h8s_smem_doubles(const Dims& d) {
   constexpr int NWS = MAXT <= 256 ? 8 : 16;
-  return (PREFETCH ? 4L : SD_SMEM ? 3L : 2L) * d.nb * 64 + 2L * (d.nb + 2) * 8 + 3 * NWS;
+  const long R = (d.nb + CL - 1) / CL;  // block rows per CTA
+  return (PREFETCH ? 4L : SD_SMEM ? 3L : 2L) * R * 64 + (R + 2) * 8 + (R + 2 + (CL > 1)) * 8 + 3L * NWS * CL;
 }
 
 /// MAXT = 256: 255 registers per thread; with PREFETCH = false (T <= 127) the
@@ -113,7 +114,15 @@ __device__ unsigned long long g_h8s_clk[16];
 /// third shared-memory region as well, so only L_i's rows stay in registers:
 /// the > 8-warp forms (168 registers per thread) then run without spilling
 /// where three regions fit (T <= 134).
-template <int MAXT, bool PREFETCH, bool PD_SMEM = false, bool SD_SMEM = false>
+/// CL > 1 (long horizons, FAST, no prefetch): a thread-block cluster of CL
+/// CTAs solves one problem, CTA c holding block rows [cR, cR + R) of every
+/// region with this kernel's register residency. Neighbour rows across a CTA
+/// boundary exchange x and the hand-overs through distributed shared memory
+/// (halo slots: vbuf R + 1 <- the next CTA's first row; xbuf 1 and 0 <- the
+/// previous CTA's last row, for the Phi^-1 and the (-S) products), every
+/// warp's dot partial goes to every CTA, and the product and dot barriers
+/// become cluster barriers.
+template <int MAXT, bool PREFETCH, bool PD_SMEM = false, bool SD_SMEM = false, int CL = 1>
 __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, const int* __restrict__ n_work,
                                          int* __restrict__ counter, double* __restrict__ sol_all, double epsilon,
                                          int max_iters_cfg) {
@@ -123,10 +132,15 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   const Dims d = v.d;
   const int nl = d.nl, nb = d.nb;
   const int tid = threadIdx.x;
-  const int R = nb;
+  static_assert(CL == 1 || (!PREFETCH && !SD_SMEM), "the cluster form is a no-prefetch form");
+  const int crank = CL == 1 ? 0 : static_cast<int>(cooperative_groups::this_cluster().block_rank());
+  const int R = CL == 1 ? nb : (nb + CL - 1) / CL;  // block rows per CTA
+  const int row0 = crank * R;                        // first global block row of this CTA
+  const int nrows = CL == 1 ? nb : max(0, min(R, nb - row0));
+  const int nsub = CL == 1 ? nb - 1 : max(0, min(R, nb - 1 - row0));
   const int il = tid >> 1, h = tid & 1;
-  const int i = il;
-  const bool act = i < nb;
+  const int i = row0 + il;  // global block row
+  const bool act = il < nrows;
   const bool has_next = act && i + 1 < nb;
   const bool has_prev = i > 0;
   const int lane = tid & 31, warp = tid >> 5;
@@ -146,8 +160,8 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   double* sNd = PREFETCH ? sPu + R * 64 : SD_SMEM ? sSr : sPd;
   double* sNs = SD_SMEM ? sPd : sNd + R * 64;
   double* vbuf = sPu + (PREFETCH ? 3 : SD_SMEM ? 2 : 1) * R * 64;  // [R + 2] x_i halves (slot = row + 1)
-  double* xbuf = vbuf + (R + 2) * 8;
-  double* red = xbuf + (R + 2) * 8;  // [3][NWS] dot partials
+  double* xbuf = vbuf + (R + 2) * 8;  // hand-overs (CL > 1: one more halo slot in front)
+  double* red = xbuf + (R + 2 + (CL > 1)) * 8;  // [3][CL][NWS] dot partials
 
   const int p = i & 1, m = (i >> 1) & 1;
   h8f::Bases bs;
@@ -157,7 +171,9 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     for (int j = 0; j < 2; ++j)
       bs.o[k][j] = ((k & 1) ? -8 * p : 8 * p) + 4 * ((k >> 1) ? 1 - h : h) + 2 * (j ^ m);
 
-  const int ib = act ? il : nb - 1;
+  // local block of this row (inactive rows: the last one)
+  const int ib = CL == 1 ? (act ? il : nb - 1) : (act ? il : max(0, nrows - 1));
+  const int gb = row0 + ib;                      // its global index (the record's swizzle)
   const int io = has_next ? il : 0;
   const double* PdI = sPd + ib * 64;
   const double* PuI = sPu + io * 64;
@@ -174,7 +190,19 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   // same thread has just read (row 0 reads slot 0, masked by has_prev)
   const int pp0 = voff(max(sv - 2, 0), 2 * h), pp1 = voff(max(sv - 2, 0), 2 * h + 1);
   const int nf0 = voff(sv + 1, 0), nf1 = voff(sv + 1, 1), nf2 = voff(sv + 1, 2), nf3 = voff(sv + 1, 3);
-  const uint32_t bd = static_cast<uint32_t>(nb) * 512u, bo = static_cast<uint32_t>(nb - 1) * 512u;
+  // hand-over slots: CL > 1 shifts them one up so that the (-S) product's
+  // (one slot lower) has a halo slot for row 0 too
+  constexpr int XS = CL > 1 ? 1 : 0;
+  const int xmy0 = CL == 1 ? my0 : voff(sv + XS, 2 * h), xmy1 = CL == 1 ? my1 : voff(sv + XS, 2 * h + 1);
+  const int xpv0 = CL == 1 ? pv0 : voff(sv - 1 + XS, 2 * h), xpv1 = CL == 1 ? pv1 : voff(sv - 1 + XS, 2 * h + 1);
+  const int xpp0 = CL == 1 ? pp0 : voff(max(sv - 2 + XS, 0), 2 * h);
+  const int xpp1 = CL == 1 ? pp1 : voff(max(sv - 2 + XS, 0), 2 * h + 1);
+  // halos: my x half -> slot sv + R of the previous CTA (my first row), my
+  // hand-overs -> slot (their slot) - R of the next CTA (my last row)
+  const bool to_prev = CL > 1 && act && il == 0 && crank > 0;
+  const bool to_next = CL > 1 && act && il == R - 1 && crank < CL - 1;
+  const uint32_t bd = static_cast<uint32_t>(CL == 1 ? nb : nrows) * 512u;
+  const uint32_t bo = static_cast<uint32_t>(CL == 1 ? nb - 1 : nsub) * 512u;
 
   // next work item and its problem index (tid 0 only). Problems that failed
   // earlier are skipped at the start of their turn (all threads read the
@@ -184,21 +212,29 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     s_next = w;
     s_pidx = w < nwk ? work[w] : 0;
   };
-  auto stage_s = [&](int pi) {  // -S blocks of problem pi -> staging area
+  auto stage_s = [&](int pi) {  // -S blocks of problem pi (this CTA's rows) -> staging area
     const double* rec = v.blocks + static_cast<long>(pi) * d.blk_stride;
+    if constexpr (CL > 1) rec += static_cast<long>(row0) * 64;
     mbar_arrive_expect_tx(&s_bar[0], bd + bo);
-    tma_bulk_g2s(sNd, rec + d.s_diag, bd, &s_bar[0]);
+    if (CL == 1 || bd) tma_bulk_g2s(sNd, rec + d.s_diag, bd, &s_bar[0]);
     if (bo) tma_bulk_g2s(sNs, rec + d.s_sub, bo, &s_bar[0]);
   };
 
-  if (tid < 3 * NWS) red[tid] = 0.0;
+  if constexpr (CL == 1) {
+    if (tid < 3 * NWS) red[tid] = 0.0;
+  } else {
+    for (int k = tid; k < 3 * NWS * CL; k += blockDim.x) red[k] = 0.0;
+  }
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
-    grab();
-    if (PREFETCH && s_next < nwk) stage_s(s_pidx);
+    if constexpr (CL == 1) {
+      grab();
+      if (PREFETCH && s_next < nwk) stage_s(s_pidx);
+    }
   }
   __syncthreads();
+  if constexpr (CL > 1) h8f_sync<CL>();  // every CTA of the cluster running (and its red zeroed) before any remote access
   uint32_t phase = 0, ph1 = 0;  // parities of s_bar[0] (staging) and s_bar[1] (Phi^-1)
   const int max_iters = max_iters_cfg > 0 ? max_iters_cfg : 2 * nl;
   const double threshold = epsilon * epsilon;
@@ -207,11 +243,19 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     double s = fma(a[3], b[3], fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0])));
     s = act ? s : 0.0;
     s = warp_sum(s);
-    if (lane == 0) red[slot * NWS + warp] = s;
+    if (lane == 0) {
+      if constexpr (CL == 1) {
+        red[slot * NWS + warp] = s;
+      } else {
+        const int at = (slot * CL + crank) * NWS + warp;
+#pragma unroll
+        for (int c = 0; c < CL; ++c) cooperative_groups::this_cluster().map_shared_rank(red, c)[at] = s;
+      }
+    }
   };
   // pairwise over the 8 warp slots (slots of absent warps hold 0): depth 3
-  auto total = [&](int slot) -> double {
-    const double2* q = reinterpret_cast<const double2*>(red + slot * NWS);
+  auto total1 = [&](const double* base) -> double {
+    const double2* q = reinterpret_cast<const double2*>(base);
     const double2 a = q[0], b = q[1], c = q[2], e = q[3];
     const double t8 = ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (e.x + e.y));
     if constexpr (NWS == 8) {
@@ -221,19 +265,26 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       return t8 + (((f.x + f.y) + (g.x + g.y)) + ((k.x + k.y) + (m.x + m.y)));
     }
   };
+  // CL > 1: the CTAs' partial sums in rank order (every CTA the same bits)
+  auto total = [&](int slot) -> double {
+    double t = total1(red + slot * CL * NWS);
+#pragma unroll
+    for (int c = 1; c < CL; ++c) t = t + total1(red + (slot * CL + c) * NWS);
+    return t;
+  };
   auto dot = [&](const double* a, const double* b) -> double {
     partial(a, b, 0);
     H8S_CLK(6);
-    __syncthreads();
+    h8f_sync<CL>();
     H8S_CLK(7);
     const double t = total(0);
     H8S_CLK(8);
     return t;
   };
   auto norm = [&](const double* a) -> double {
-    __syncthreads();
+    h8f_sync<CL>();
     partial(a, a, 2);
-    __syncthreads();
+    h8f_sync<CL>();
     return sqrt(total(2));
   };
   auto gather = [&](const double* xr, double* xf) {  // x_i in logical order
@@ -287,6 +338,24 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     const double2 b = *reinterpret_cast<const double2*>(buf + o1);
     x[0] = a.x, x[1] = a.y, x[2] = b.x, x[3] = b.y;
   };
+  // CL > 1: my x half into the previous CTA's halo slot sv + R (first row)
+  auto put_halo_x = [&](const double* x) {
+    if constexpr (CL > 1)
+      if (to_prev) {
+        double* rv = cooperative_groups::this_cluster().map_shared_rank(vbuf, crank - 1);
+        *reinterpret_cast<double2*>(rv + voff(sv + R, 2 * h)) = make_double2(x[0], x[1]);
+        *reinterpret_cast<double2*>(rv + voff(sv + R, 2 * h + 1)) = make_double2(x[2], x[3]);
+      }
+  };
+  // ... and my hand-over into the next CTA's slot `slot` (last row)
+  auto put_halo_hand = [&](const double* x, int slot) {
+    if constexpr (CL > 1)
+      if (to_next) {
+        double* rx = cooperative_groups::this_cluster().map_shared_rank(xbuf, crank + 1);
+        *reinterpret_cast<double2*>(rx + voff(slot, 2 * h)) = make_double2(x[0], x[1]);
+        *reinterpret_cast<double2*>(rx + voff(slot, 2 * h + 1)) = make_double2(x[2], x[3]);
+      }
+  };
   auto finish = [&](const double* own, const double* low, const double* up, double* out) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // diag, then sub (i > 0), then super (i < nb - 1)
@@ -301,6 +370,18 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
   double2 so[8][2];  // my rows of L_i
 
   for (;;) {
+    if constexpr (CL > 1) {  // the cluster's next problem, taken by CTA 0 for all
+      if (tid == 0 && crank == 0) {
+        const int wk = atomicAdd(counter, 1);
+        const int pk = wk < nwk ? work[wk] : 0;
+#pragma unroll
+        for (int c = 0; c < CL; ++c) {
+          *cooperative_groups::this_cluster().map_shared_rank(&s_next, c) = wk;
+          *cooperative_groups::this_cluster().map_shared_rank(&s_pidx, c) = pk;
+        }
+      }
+      h8f_sync<CL>();
+    }
     const int w = s_next;
     if (w >= nwk) break;
     const int pidx = s_pidx;
@@ -318,9 +399,13 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     const bool runnable = v.status[pidx].code == DOCP_OK;  // failed in an earlier stage: skip
     if constexpr (!PREFETCH) {
       if (!runnable) {  // block-uniform
-        __syncthreads();  // s_next / s_pidx read by every thread
-        if (tid == 0) grab();
-        __syncthreads();
+        if constexpr (CL > 1) {
+          h8f_sync<CL>();  // s_next / s_pidx read in every CTA
+        } else {
+          __syncthreads();  // s_next / s_pidx read by every thread
+          if (tid == 0) grab();
+          __syncthreads();
+        }
         continue;
       }
       if (tid == 0) {  // this problem's -S into the record region (free since the last barrier)
@@ -329,7 +414,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       }
     }
     mbar_wait(&s_bar[0], phase);
-    if constexpr (!SD_SMEM) h8s::load_sym(NdI, ib, h, sd);
+    if constexpr (!SD_SMEM) h8s::load_sym(NdI, gb, h, sd);
     h8f::load_rows(NsI, bs, so);
     __syncthreads();  // staging area consumed; s_next / s_pidx read; Phi^-1 reads of the previous problem done
     phase ^= 1;
@@ -347,11 +432,14 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     if (tid == 0) {
       fence_proxy_async();
       const double* rec = v.blocks + static_cast<long>(pidx) * d.blk_stride;
+      if constexpr (CL > 1) rec += static_cast<long>(row0) * 64;
       mbar_arrive_expect_tx(&s_bar[1], bd + bo);
-      tma_bulk_g2s(sPd, rec + d.p_diag, bd, &s_bar[1]);
+      if (CL == 1 || bd) tma_bulk_g2s(sPd, rec + d.p_diag, bd, &s_bar[1]);
       if (bo) tma_bulk_g2s(sPu, rec + d.p_sup, bo, &s_bar[1]);
-      grab();  // s_next / s_pidx: read after the end-of-problem barrier
-      if (PREFETCH && s_next < nwk) stage_s(s_pidx);
+      if constexpr (CL == 1) {
+        grab();  // s_next / s_pidx: read after the end-of-problem barrier
+        if (PREFETCH && s_next < nwk) stage_s(s_pidx);
+      }
     }
 
     double lam[4] = {l01.x, l01.y, l23.x, l23.y}, r[4] = {0, 0, 0, 0}, pv[4], y[4];
@@ -362,6 +450,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       double xf[8], own[4], hand[4], low[4], up[4], xn[4];
       gather(xr, xf);
       put(vbuf, my0, my1, xr);
+      put_halo_x(xr);
       H8S_CLK(12);
       if constexpr (SD_SMEM) {
         double2 dd[8][2];
@@ -372,15 +461,16 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       }
       H8S_CLK(13);
       rows_times(so, xf, hand);  // L_i x_i
-      put(xbuf, pv0, pv1, hand);  // slot i (see pp0 above)
+      put(xbuf, xpv0, xpv1, hand);  // slot i (see pp0 above)
+      put_halo_hand(hand, sv - 1 + XS - R);
       H8S_CLK(14);
       partial(a, b, slot);
       H8S_CLK(0);
-      __syncthreads();
+      h8f_sync<CL>();
       H8S_CLK(1);
       get(vbuf, nx0, nx1, xn);
       trans_times(so, xn, up);   // L_i' x_{i+1}
-      get(xbuf, pp0, pp1, low);
+      get(xbuf, xpp0, xpp1, low);
       finish(own, low, up, out);
     };
     // out = Phi^-1 x from shared memory. Two exchanges (x_{i+1}, then the
@@ -391,6 +481,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       double xf[8], own[4], hand[4], low[4], up[4], xn[8];
       gather(xr, xf);
       put(vbuf, my0, my1, xr);
+      put_halo_x(xr);
       if constexpr (PD_SMEM) {
         double2 dd[8][2];
         h8f::load_rows(PdI, bs, dd);
@@ -399,7 +490,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
         h8s::sym_times(pd, xf, xr, h, own);
       }
       H8S_CLK(3);
-      __syncthreads();
+      h8f_sync<CL>();
       H8S_CLK(1);
       get(vbuf, nf0, nf1, xn);
       get(vbuf, nf2, nf3, xn + 4);
@@ -409,11 +500,12 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
         trans_times(oo, xr, hand);  // U_i' x_i
         rows_times(oo, xn, up);     // U_i x_{i+1}
       }
-      put(xbuf, my0, my1, hand);
+      put(xbuf, xmy0, xmy1, hand);
+      put_halo_hand(hand, sv + XS - R);
       H8S_CLK(4);
-      __syncthreads();
+      h8f_sync<CL>();
       H8S_CLK(1);
-      get(xbuf, pv0, pv1, low);
+      get(xbuf, xpv0, xpv1, low);
       finish(own, low, up, out);
     };
 
@@ -423,10 +515,10 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
     } else {
       r[0] = r[1] = r[2] = r[3] = 0.0;
     }
-    __syncthreads();  // every phase-2 read of lambda / its hand-over is done
+    h8f_sync<CL>();  // every phase-2 read of lambda / its hand-over is done
     mbar_wait(&s_bar[1], ph1);
     ph1 ^= 1;
-    if constexpr (!PD_SMEM) h8s::load_sym(PdI, ib, h, pd);
+    if constexpr (!PD_SMEM) h8s::load_sym(PdI, gb, h, pd);
     double rt[4], sr[4];  // r~ and (-S) r~
     matvec_p(r, rt);                 // r~ = Phi^-1 r
     // Pipelined second dot: sr = (-S) r~ is formed while eta = r'r~ reduces
@@ -489,7 +581,7 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       *reinterpret_cast<double2*>(sol + i * 8 + 4 * h) = make_double2(lam[0], lam[1]);
       *reinterpret_cast<double2*>(sol + i * 8 + 4 * h + 2) = make_double2(lam[2], lam[3]);
     }
-    if (tid == 0) {
+    if (tid == 0 && crank == 0) {
       v.pcg_iters[pidx] = iters;
       v.final_eta[pidx] = eta;
       v.pcg_conv[pidx] = status == DOCP_OK && eta <= threshold;
@@ -499,7 +591,9 @@ __device__ __forceinline__ void h8s_body(View v, const int* __restrict__ work, c
       atomicAdd(v.pcg_acc + 1, 1ull);
       atomicAdd(v.pcg_acc + 2, 1ull);  // lifetime solves (docp_pcg_invocations)
     }
-    __syncthreads();  // s_next is published; Phi^-1 / vectors free for the next problem
+    // s_next is published; Phi^-1 / vectors (and, CL > 1, the halos) free for the next problem
+    if constexpr (CL > 1) h8f_sync<CL>();
+    else __syncthreads();
   }
 #ifdef DOCP_H8S_CLOCK
   if (tid == 0)
@@ -513,6 +607,16 @@ __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8s(View v, const int* __r
                                                         double* __restrict__ sol_all, double epsilon,
                                                         int max_iters_cfg) {
   h8s_body<MAXT, PREFETCH>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
+}
+
+/// Long horizons (T > 191): a cluster of CL CTAs of <= 8 warps each, the
+/// blocks register- and shared-memory-resident across them.
+template <int CL>
+__global__ void __launch_bounds__(256, 1) pcg_kernel_h8s_cl(View v, const int* __restrict__ work,
+                                                           const int* __restrict__ n_work, int* __restrict__ counter,
+                                                           double* __restrict__ sol_all, double epsilon,
+                                                           int max_iters_cfg) {
+  h8s_body<256, false, false, false, CL>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
 }
 
 /// Up to 384 threads (T <= 191): 9-12 warps, so an SMSP holds three of them

@@ -74,6 +74,73 @@ int launch_h8f_cl(docp_batch* b, const int* list, const int* count, int n_hint, 
   return DOCP_OK;
 }
 
+/// FAST, device-assembled systems beyond one SM (T > 191): pcg_kernel_h8s_cl
+/// on a cluster of CL CTAs (h8s's register residency, rows split over the
+/// cluster). Returns -1 (nothing launched) when the shape does not fit.
+template <int CL>
+static int launch_h8s_cl(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
+                         int max_iters) {
+  auto kern = pcg_kernel_h8s_cl<CL>;
+  const int R = (b->d.nb + CL - 1) / CL;
+  const int threads = (2 * R + 31) / 32 * 32;
+  if (threads > 256) return -1;
+  const size_t smem = h8s_smem_doubles<256, false, false, CL>(b->d) * sizeof(double);
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device);
+  if (smem + 256 > static_cast<size_t>(max_optin)) return -1;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  cudaLaunchConfig_t lc{};
+  cudaLaunchAttribute attr[1];
+  lc.blockDim = dim3(threads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = b->stream;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  lc.gridDim = dim3(CL * b->num_sms);
+  int groups = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveClusters(&groups, kern, &lc));
+  if (groups < 1) return -1;
+  lc.gridDim = dim3(CL * std::max(1, std::min(n_hint, groups)));
+  CUDA_TRY(cudaMemsetAsync(b->counts + 3, 0, sizeof(int), b->stream));
+  ProfScope ps(b, DOCP_PROF_PCG);
+  CUDA_TRY(cudaLaunchKernelEx(&lc, kern, b->v, list, count, b->counts + 3, sol, eps, max_iters));
+  LAUNCH_CHECK();
+  return DOCP_OK;
+}
+
+/// Smallest cluster (2 .. 8) for pcg_kernel_h8s_cl: <= 128 block rows (8
+/// warps) per CTA, every CTA owning a row, two record regions per CTA in
+/// shared memory; 0 if none.
+int h8s_cluster_for(const Dims& d, int device) {
+  if (d.nx != 8) return 0;
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  for (int cl = 2; cl <= 8; ++cl) {
+    const int R = (d.nb + cl - 1) / cl;
+    if ((cl - 1) * R >= d.nb) break;
+    if (R > 128) continue;
+    const long doubles = 2L * R * 64 + (R + 2) * 8 + (R + 3) * 8 + 3L * 8 * cl;
+    if (doubles * 8 + 256 <= static_cast<long>(max_optin)) return cl;
+  }
+  return 0;
+}
+
+/// Whether long-horizon FAST solves of device-assembled systems take the
+/// register-resident cluster form over the shared-memory one (h8f): when it
+/// needs fewer CTAs per problem, or at two (measured at B = 4,096: T = 200
+/// 111K vs 104K problems/s, T = 240 103K vs 69K, T = 320 60K vs 46K; at an
+/// equal cluster of 3 or 4 h8f is within +-5 %, ahead at T = 256).
+bool h8s_cluster_preferred(const Dims& d, int device) {
+  const int cs = h8s_cluster_for(d, device);
+  if (cs == 0) return false;
+  const int cf = h8f_cluster_for(d, device);
+  return cf == 0 || cs < cf || cs == 2;
+}
+
 /// FAST, one CTA per problem: pcg_kernel_h8r (-S in registers, next
 /// problem's -S prefetched into shared memory).
 static int launch_h8r(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
@@ -244,6 +311,21 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
       default: break;
     }
     if (rc != -1) return rc;
+    // beyond one SM: the same residency on a thread-block cluster (DOCP_PCG_VARIANT=h8f: the
+    // shared-memory cluster form instead)
+    if (var == 0 && !force_variant("h8f_cl") && h8s_cluster_preferred(b->d, b->device)) {
+      switch (h8s_cluster_for(b->d, b->device)) {
+        case 2: rc = launch_h8s_cl<2>(b, list, count, n_hint, sol, eps, max_iters); break;
+        case 3: rc = launch_h8s_cl<3>(b, list, count, n_hint, sol, eps, max_iters); break;
+        case 4: rc = launch_h8s_cl<4>(b, list, count, n_hint, sol, eps, max_iters); break;
+        case 5: rc = launch_h8s_cl<5>(b, list, count, n_hint, sol, eps, max_iters); break;
+        case 6: rc = launch_h8s_cl<6>(b, list, count, n_hint, sol, eps, max_iters); break;
+        case 7: rc = launch_h8s_cl<7>(b, list, count, n_hint, sol, eps, max_iters); break;
+        case 8: rc = launch_h8s_cl<8>(b, list, count, n_hint, sol, eps, max_iters); break;
+        default: break;
+      }
+      if (rc != -1) return rc;
+    }
   }
   if (!par && !force_h8()) {
     switch (h8f_cluster(b)) {

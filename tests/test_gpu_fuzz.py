@@ -17,7 +17,7 @@ RTOL_FAST = 1e-9
 
 # (n_x, n_u, T): every PCG / K1 variant, including cluster sizes 2, 3, 4, 5, 6, 7, 8 for n_x = 8
 SHAPES = [(1, 1, 3), (2, 1, 9), (3, 3, 17), (4, 1, 50), (4, 2, 20), (5, 2, 33), (6, 2, 64), (7, 3, 25),
-          (8, 2, 100), (8, 4, 1), (8, 4, 2), (8, 4, 113), (8, 4, 114), (8, 4, 200), (8, 4, 256), (8, 4, 400), (8, 4, 512), (8, 4, 600), (8, 4, 700), (8, 4, 800),
+          (8, 2, 100), (8, 4, 1), (8, 4, 2), (8, 4, 113), (8, 4, 114), (8, 4, 200), (8, 4, 240), (8, 4, 256), (8, 4, 320), (8, 4, 400), (8, 4, 512), (8, 4, 600), (8, 4, 700), (8, 4, 800),
           (9, 2, 40), (12, 4, 20), (16, 8, 6), (16, 8, 60)]
 
 

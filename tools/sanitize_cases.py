@@ -24,6 +24,8 @@ CASES = {
     "h8f_cl1": (8, 4, 30, 3, {"DOCP_PCG_VARIANT": "h8f"}, ("fast",)),
     "h8f_cl2": (8, 4, 60, 2, {"DOCP_PCG_VARIANT": "h8f", "DOCP_H8F_CLUSTER": "2"}, ("fast",)),
     "h8f_cl3": (8, 4, 60, 2, {"DOCP_PCG_VARIANT": "h8f", "DOCP_H8F_CLUSTER": "3"}, ("fast",)),
+    "h8s_cl2": (8, 4, 200, 2, {}, ("fast",)),
+    "h8s_cl3": (8, 4, 320, 1, {}, ("fast",)),
     "h8f_cl4": (8, 4, 60, 2, {"DOCP_PCG_VARIANT": "h8f", "DOCP_H8F_CLUSTER": "4"}, ("fast",)),
     "h8f_cl6": (8, 4, 60, 2, {"DOCP_PCG_VARIANT": "h8f", "DOCP_H8F_CLUSTER": "6"}, ("fast",)),
     "h8f_cl4_nodbuf": (8, 4, 400, 1, {}, ("fast",)),  # R = 101: the barrier form (no second buffer pair)
