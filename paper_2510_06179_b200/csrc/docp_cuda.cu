@@ -1106,7 +1106,7 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   else if (s8 >= 2) snprintf(fast, sizeof fast, "pcg_kernel_h8s<%d,no-prefetch%s>(resident); uploaded systems %s",
                              s8 == 2 ? 256 : 384, s8 == 4 ? ",-S in smem" : "",
                              cl == 2 ? "pcg_kernel_h8f(cluster2)" : "pcg_kernel_h8f");
-  else if (d.nx == 8 && h8s_cluster_preferred(d, dev))
+  else if (d.nx == 8 && s8 == 0 && h8s_cluster_preferred(d, dev))
     snprintf(fast, sizeof fast, "pcg_kernel_h8s_cl(cluster%d,resident); uploaded systems pcg_kernel_h8f",
              h8s_cluster_for(d, dev));
   else if (cl == 1) snprintf(fast, sizeof fast, "%s(resident)",
