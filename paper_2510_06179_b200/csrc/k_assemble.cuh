@@ -683,20 +683,27 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
           __syncwarp(gmask);
           K1_CLK(2);
           // column l of chi = A M1 + B M2 + A+ Q+^-1 A+'  and of phi_t = A Q_t^-1
+          // (the lane's columns of M1 and M2 in registers: the stores into sC
+          // below would otherwise force their reload for every row)
+          double m1[NX], m2[NU];
+#pragma unroll
+          for (int m = 0; m < NX; ++m) m1[m] = sM1[ix(m, l)];
+#pragma unroll
+          for (int m = 0; m < NU; ++m) m2[m] = sM2[iu(m, l)];
 #pragma unroll
           for (int i = 0; i < NX; ++i) {
-            double a = sA[ix(i, 0)] * sM1[ix(0, l)];
-            double b = sB[ix(i, 0)] * sM2[iu(0, l)];
+            double a = sA[ix(i, 0)] * m1[0];
+            double b = sB[ix(i, 0)] * m2[0];
             if constexpr (FAST) {
 #pragma unroll
-              for (int m = 1; m < NX; ++m) a = fma(sA[ix(i, m)], sM1[ix(m, l)], a);
+              for (int m = 1; m < NX; ++m) a = fma(sA[ix(i, m)], m1[m], a);
 #pragma unroll
-              for (int m = 1; m < NU; ++m) b = fma(sB[ix(i, m)], sM2[iu(m, l)], b);
+              for (int m = 1; m < NU; ++m) b = fma(sB[ix(i, m)], m2[m], b);
             } else {
 #pragma unroll
-              for (int m = 1; m < NX; ++m) a = a + sA[ix(i, m)] * sM1[ix(m, l)];
+              for (int m = 1; m < NX; ++m) a = a + sA[ix(i, m)] * m1[m];
 #pragma unroll
-              for (int m = 1; m < NU; ++m) b = b + sB[ix(i, m)] * sM2[iu(m, l)];
+              for (int m = 1; m < NU; ++m) b = b + sB[ix(i, m)] * m2[m];
             }
             sC[ix(i, l)] = (a + b) + (i == l ? c3 : 0.0);
           }
@@ -825,20 +832,26 @@ __global__ void __launch_bounds__(TH, NX >= 16 ? 2 : (TH > 128 ? 3 : 4)) assembl
           __syncwarp(gmask);
           Pt = sA;
         }
-        // T1(i, l) = sum_m (-P_t(i,m)) sub_t(l,m)
+        // T1(i, l) = sum_m (-P_t(i,m)) sub_t(l,m); row l of sub_t and column
+        // l of P_{t+1} in registers (the stores in between would force reloads)
+        double sub[NX], pn[NX];
+#pragma unroll
+        for (int m = 0; m < NX; ++m) sub[m] = sM1[ix(l, m)];
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
-          double a = (-Pt[ix(i, 0)]) * sM1[ix(l, 0)];
+          double a = (-Pt[ix(i, 0)]) * sub[0];
 #pragma unroll
-          for (int m = 1; m < NX; ++m) a = FAST ? fma(-Pt[ix(i, m)], sM1[ix(l, m)], a) : a + (-Pt[ix(i, m)]) * sM1[ix(l, m)];
+          for (int m = 1; m < NX; ++m) a = FAST ? fma(-Pt[ix(i, m)], sub[m], a) : a + (-Pt[ix(i, m)]) * sub[m];
           sC[ix(i, l)] = a;
         }
+#pragma unroll
+        for (int m = 0; m < NX; ++m) pn[m] = sD[ix(m, l)];
         __syncwarp(gmask);
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
-          double a = sC[ix(i, 0)] * sD[ix(0, l)];
+          double a = sC[ix(i, 0)] * pn[0];
 #pragma unroll
-          for (int m = 1; m < NX; ++m) a = FAST ? fma(sC[ix(i, m)], sD[ix(m, l)], a) : a + sC[ix(i, m)] * sD[ix(m, l)];
+          for (int m = 1; m < NX; ++m) a = FAST ? fma(sC[ix(i, m)], pn[m], a) : a + sC[ix(i, m)] * pn[m];
           stage(t, i, l, a);
         }
         flush(Pu, t);
