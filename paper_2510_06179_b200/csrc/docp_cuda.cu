@@ -1115,7 +1115,7 @@ int docp_describe(const docp_problem* p, char* buf, int32_t cap) {
   else snprintf(fast, sizeof fast, "%s", d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
                                                    : d.nx == 4 ? "pcg_kernel<4>" : (d.nx == 6 || d.nx == 9) ? "pcg_kernel<NX=6|9>" : "pcg_kernel<runtime>");
   const int p8 = d.nx == 8 ? h8p_variant_for(d, dev) : 0;
-  const char* parity = p8 == 1   ? "pcg_kernel_h8p<prefetch>; uploaded systems pcg_kernel_h8"
+  const char* parity = p8 == 1   ? "pcg_kernel_h8p<-S resident>; uploaded systems pcg_kernel_h8"
                        : p8 == 2 ? "pcg_kernel_h8p<no-prefetch>; uploaded systems pcg_kernel_h8"
                        : d.nx == 8 ? (2 * d.nb <= 512 ? "pcg_kernel_h8" : "pcg_kernel<8>")
                                    : d.nx == 4 ? "pcg_kernel<4>" : (d.nx == 6 || d.nx == 9) ? "pcg_kernel<NX=6|9>" : "pcg_kernel<runtime>";

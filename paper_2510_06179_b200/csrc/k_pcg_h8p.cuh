@@ -188,7 +188,11 @@ __device__ unsigned long long g_h8p_clk[16];
 /// CW: a CTA of 8 warps whose last warp holds no block rows (T <= 111) folds
 /// the block dots there (one extra barrier per dot, the fold from registers).
 constexpr int CW_WARP = 7;
-template <int MAXT, bool PREFETCH, bool CW = false>
+/// SDS: -S_ii stays in shared memory for the solve (a fourth region instead
+/// of the next problem's prefetch): the (-S) diagonal product reads full rows
+/// there (no partner exchange, no packed share in registers), at the price of
+/// exposing the record load at each problem's start.
+template <int MAXT, bool PREFETCH, bool CW = false, bool SDS = false>
 __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, const int* __restrict__ n_work,
                                          int* __restrict__ counter, double* __restrict__ sol_all, double epsilon,
                                          int max_iters_cfg) {
@@ -211,11 +215,12 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
   long long clk[12] = {0}, t_last = clock64();
 #endif
 
-  double* sPd = sm_pcg;        // [R] Phi^-1 diagonal blocks (current problem; staging only)
-  double* sPu = sPd + R * 64;  // [R] Phi^-1 super blocks
-  double* sNd = PREFETCH ? sPu + R * 64 : sPd;
+  static_assert(!(SDS && PREFETCH), "SDS keeps -S of the current problem where the prefetch would land");
+  double* sPd = SDS ? sm_pcg + 2 * R * 64 : sm_pcg;  // [R] Phi^-1 diagonal blocks
+  double* sPu = sPd + R * 64;                        // [R] Phi^-1 super blocks
+  double* sNd = SDS ? sm_pcg : (PREFETCH ? sPu + R * 64 : sPd);  // -S diagonal blocks (staging, or resident: SDS)
   double* sNs = sNd + R * 64;
-  double* vbuf = sPu + (PREFETCH ? 3 : 1) * R * 64;  // [R + 2] x_i (slot = row + 1)
+  double* vbuf = (SDS || PREFETCH) ? sm_pcg + 4 * R * 64 : sPu + R * 64;  // [R + 2] x_i (slot = row + 1)
   double* xbuf = vbuf + (R + 2) * 8;                 // [R + 2] hand-overs
   double* seg = xbuf + (R + 2) * 8;                  // [h8p_seg_doubles] block dots, zero past nb
 
@@ -238,6 +243,7 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
   const int b1 = blk_off(8, io, 4 * h, 0), b2 = blk_off(8, io, 4 * (1 - h), 4);
   // Phi^-1_ii: column 4h + q, rows 2k.. at bdg ^ (8 q + 2 k) (same identity, block ib)
   const double* PdI = sPd + ib * 64;
+  const double* SdI = sNd + ib * 64;  // SDS: -S_ii resident (same tile offsets as Phi^-1_ii)
   const int bdg = blk_off(8, ib, 0, 4 * h);
   auto grab = [&]() {
     const int w = atomicAdd(counter, 1);
@@ -409,10 +415,16 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
       if (tid == 0) {
         fence_proxy_async();
         stage_s(pidx);
+        if constexpr (SDS) {  // Phi^-1 has its own regions: load it now too
+          const double* rec = v.blocks + static_cast<long>(pidx) * d.blk_stride;
+          mbar_arrive_expect_tx(&s_bar[1], bd + bo);
+          tma_bulk_g2s(sPd, rec + d.p_diag, bd, &s_bar[1]);
+          if (bo) tma_bulk_g2s(sPu, rec + d.p_sup, bo, &s_bar[1]);
+        }
       }
     }
     mbar_wait(&s_bar[0], phase);
-    h8p::load_symp(sNd + ib * 64, ib, h, sd);
+    if constexpr (!SDS) h8p::load_symp(sNd + ib * 64, ib, h, sd);
     h8p::load_quarters(sNs + io * 64, io, h, lq);
     __syncthreads();  // staging area consumed; s_next / s_pidx read; previous Phi^-1 reads done
     phase ^= 1;
@@ -428,11 +440,13 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
       }
     }
     if (tid == 0) {
-      fence_proxy_async();
-      const double* rec = v.blocks + static_cast<long>(pidx) * d.blk_stride;
-      mbar_arrive_expect_tx(&s_bar[1], bd + bo);
-      tma_bulk_g2s(sPd, rec + d.p_diag, bd, &s_bar[1]);
-      if (bo) tma_bulk_g2s(sPu, rec + d.p_sup, bo, &s_bar[1]);
+      if constexpr (!SDS) {
+        fence_proxy_async();
+        const double* rec = v.blocks + static_cast<long>(pidx) * d.blk_stride;
+        mbar_arrive_expect_tx(&s_bar[1], bd + bo);
+        tma_bulk_g2s(sPd, rec + d.p_diag, bd, &s_bar[1]);
+        if (bo) tma_bulk_g2s(sPu, rec + d.p_sup, bo, &s_bar[1]);
+      }
       grab();
       if (PREFETCH && s_next < nwk) stage_s(s_pidx);
     }
@@ -449,7 +463,31 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
       gather(xr, xf);
       put(vbuf, my0, my1, xr);
       h8p::first_halves(lq.f, xf, hf);
-      h8p::phase1_fold(sd, xf, h, hf, lq.g, own, hs);
+      if constexpr (SDS) {
+        // own rows of -S_ii x from shared memory (row 4h + q = column 4h + q): full folds
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double col[8];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double2 a = *reinterpret_cast<const double2*>(SdI + (bdg ^ (8 * q + 2 * k)));
+            col[2 * k] = a.x, col[2 * k + 1] = a.y;
+          }
+          double acc = col[0] * xf[0];
+#pragma unroll
+          for (int c = 1; c < 8; ++c) acc = acc + col[c] * xf[c];
+          own[q] = acc;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // hand-over second halves after the partner's first halves
+          double acc = __shfl_xor_sync(0xffffffffu, hf[q], 1);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc = acc + lq.g[q][c] * xf[4 + c];
+          hs[q] = acc;
+        }
+      } else {
+        h8p::phase1_fold(sd, xf, h, hf, lq.g, own, hs);
+      }
       put(xbuf, ho0, ho1, hs);
       H8P_CLK(0);
       __syncthreads();
@@ -608,12 +646,12 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
 #endif
 }
 
-template <int MAXT, bool PREFETCH, bool CW = false>
+template <int MAXT, bool PREFETCH, bool CW = false, bool SDS = false>
 __global__ void __launch_bounds__(MAXT, 1) pcg_kernel_h8p(View v, const int* __restrict__ work,
                                                         const int* __restrict__ n_work, int* __restrict__ counter,
                                                         double* __restrict__ sol_all, double epsilon,
                                                         int max_iters_cfg) {
-  h8p_body<MAXT, PREFETCH, CW>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
+  h8p_body<MAXT, PREFETCH, CW, SDS>(v, work, n_work, counter, sol_all, epsilon, max_iters_cfg);
 }
 
 }  // namespace docp_dev

@@ -188,15 +188,22 @@ static int launch_h8s(docp_batch* b, const int* list, const int* count, int n_hi
 /// PARITY, one CTA per problem, device-assembled (symmetric) diagonal
 /// blocks: pcg_kernel_h8p (the reference's arithmetic with h8s's residency).
 /// Returns -1 (nothing launched) when the variant does not fit this shape.
+/// SDS: -S_ii resident in shared memory instead of the next problem's
+/// prefetch (where four record regions fit, T <= 111: C3 243K -> 250K
+/// problems/s, the (-S) diagonal product without the partner exchange
+/// outweighs the exposed record load).
 template <bool PREFETCH>
 static int launch_h8p(docp_batch* b, const int* list, const int* count, int n_hint, double* sol, double eps,
-                      int max_iters) {
+                      int max_iters, bool sds = false) {
   // a spare eighth warp folds the block dots (T <= 111; DOCP_PCG_VARIANT=h8p_nocw: every warp does)
   const bool cw = 2 * b->d.nb <= 32 * CW_WARP && !force_variant("h8p_nocw");
+  sds = sds && !PREFETCH;
   auto kern = cw ? pcg_kernel_h8p<256, PREFETCH, true> : pcg_kernel_h8p<256, PREFETCH, false>;
+  if constexpr (!PREFETCH)
+    if (sds) kern = cw ? pcg_kernel_h8p<256, false, true, true> : pcg_kernel_h8p<256, false, false, true>;
   const int threads = cw ? 256 : (2 * b->d.nb + 31) / 32 * 32;
   if (threads > 256) return -1;
-  const size_t smem = h8p_smem_doubles<PREFETCH>(b->d) * sizeof(double);
+  const size_t smem = (sds ? h8p_smem_doubles<true>(b->d) : h8p_smem_doubles<PREFETCH>(b->d)) * sizeof(double);
   int max_optin = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, b->device);
   if (smem + 256 > static_cast<size_t>(max_optin)) return -1;
@@ -294,8 +301,10 @@ DOCP_PCG_LAUNCHER(launch_pcg_nx8) {
   if (par && b->sym_blocks && !force_h8()) {
     int rc = -1;
     int var = h8p_variant_for(b->d, b->device);
-    if (var == 1 && force_variant("h8p_np")) var = 2;  // A/B: the no-prefetch form on a short horizon
-    if (var == 1) rc = launch_h8p<true>(b, list, count, n_hint, sol, eps, max_iters);
+    // where the prefetch form fits, the resident -S form runs instead (A/B:
+    // DOCP_PCG_VARIANT=h8p_pf the prefetch form, h8p_np the plain no-prefetch one)
+    if (var == 1 && force_variant("h8p_pf")) rc = launch_h8p<true>(b, list, count, n_hint, sol, eps, max_iters);
+    else if (var == 1) rc = launch_h8p<false>(b, list, count, n_hint, sol, eps, max_iters, !force_variant("h8p_np"));
     else if (var == 2) rc = launch_h8p<false>(b, list, count, n_hint, sol, eps, max_iters);
     if (rc != -1) return rc;
   }

@@ -63,9 +63,9 @@ def test_parity_kernels_agree_bitwise_on_c3_batch(monkeypatch):
     z0 = 0.1 * rng.standard_normal((B, nz))
     lg = rng.standard_normal((B, nz))
     out = {}
-    for variant in ("h8p", "h8"):
-        if variant == "h8":
-            monkeypatch.setenv("DOCP_PCG_VARIANT", "h8")
+    variants = ("h8p", "h8p_pf", "h8p_np", "h8")
+    for variant in variants:
+        monkeypatch.setenv("DOCP_PCG_VARIANT", "" if variant == "h8p" else variant)
         cfg = D.SqpConfig(max_sqp_iters=5, pcg=D.PcgConfig(mode="parity"))
         res, errs = D.sqp_solve_batch(prob, th, z0, np.zeros((B, nl)), cfg)
         assert all(e is None for e in errs)
@@ -73,7 +73,9 @@ def test_parity_kernels_agree_bitwise_on_c3_batch(monkeypatch):
         assert all(e is None for e in errs)
         out[variant] = (np.stack([r.z for r in res]), np.stack([r.lam for r in res]), [r.pcg_iters for r in res],
                         [r.sqp_iters for r in res], g.copy(), lt.copy(), np.asarray(its).copy())
-    a, b = out["h8p"], out["h8"]
-    assert a[2] == b[2] and a[3] == b[3] and np.array_equal(a[6], b[6])
-    for k in (0, 1, 4, 5):
-        assert np.array_equal(a[k], b[k])
+    b = out["h8"]
+    for v in variants[:-1]:
+        a = out[v]
+        assert a[2] == b[2] and a[3] == b[3] and np.array_equal(a[6], b[6]), v
+        for k in (0, 1, 4, 5):
+            assert np.array_equal(a[k], b[k]), (v, k)
