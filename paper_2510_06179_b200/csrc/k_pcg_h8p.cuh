@@ -185,9 +185,10 @@ __device__ unsigned long long g_h8p_clk[16];
 #define H8P_CLK(k)
 #endif
 
-/// CW: a CTA of 8 warps whose last warp holds no block rows (T <= 111) folds
+/// CW: a CTA whose last warp holds no block rows (T <= 111; launched with the
+/// rows' warps plus that one, so short horizons run fewer warps) folds
 /// the block dots there (one extra barrier per dot, the fold from registers).
-constexpr int CW_WARP = 7;
+constexpr int CW_WARP = 7;  // at most 7 warps of block rows (T <= 111), the fold warp after them
 /// SDS: -S_ii stays in shared memory for the solve (a fourth region instead
 /// of the next problem's prefetch): the (-S) diagonal product reads full rows
 /// there (no partner exchange, no packed share in registers), at the price of
@@ -343,7 +344,7 @@ __device__ __forceinline__ void h8p_body(View v, const int* __restrict__ work, c
     if constexpr (CW) {
       // warp 7 holds no block rows: its lane 0 folds the block dots with all
       // of them in flight at once (its registers are free), the others wait
-      if (warp == CW_WARP) {
+      if (warp == static_cast<int>(blockDim.x >> 5) - 1) {  // the last warp holds no block rows
         if (lane == 0) {
 #ifdef DOCP_H8P_CLOCK
           const long long tc0 = clock64();

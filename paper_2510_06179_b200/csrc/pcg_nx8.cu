@@ -201,7 +201,8 @@ static int launch_h8p(docp_batch* b, const int* list, const int* count, int n_hi
   auto kern = cw ? pcg_kernel_h8p<256, PREFETCH, true> : pcg_kernel_h8p<256, PREFETCH, false>;
   if constexpr (!PREFETCH)
     if (sds) kern = cw ? pcg_kernel_h8p<256, false, true, true> : pcg_kernel_h8p<256, false, false, true>;
-  const int threads = cw ? 256 : (2 * b->d.nb + 31) / 32 * 32;
+  // CW: the block rows' warps plus the fold warp (short horizons launch fewer warps)
+  const int threads = (2 * b->d.nb + 31) / 32 * 32 + (cw ? 32 : 0);
   if (threads > 256) return -1;
   const size_t smem = (sds ? h8p_smem_doubles<true>(b->d) : h8p_smem_doubles<PREFETCH>(b->d)) * sizeof(double);
   int max_optin = 0;
